@@ -1,0 +1,188 @@
+/*
+ * scrooge_b200 — C ABI of the B200-native windowed GenASM aligner.
+ *
+ * This is the drop-in boundary for the reference's aligner path
+ * (/root/reference/proj/include/scrooge/). Plain C types only; no exceptions
+ * cross it. The C++ shim (include/scrooge_b200.hpp) and the Python package
+ * (paper_2208_09985_b200) re-raise the reference's exception types from the
+ * status codes below.
+ *
+ *   reference                                       replaced by
+ *   ------------------------------------------------------------------------
+ *   AlignerConfig            aligner.hpp:12-31      sg_config
+ *   AlignerConfig::validate  aligner.cpp:8-18       sg_validate_config
+ *   align()                  aligner.hpp:45,        sg_align_batch (n_pairs = 1)
+ *                            aligner.cpp:28-85
+ *   run_batch()              batch.hpp:33-34,       sg_align_batch / sg_align_packed
+ *                            batch.cpp:13-104
+ *   PairOutcome/BatchResult  batch.hpp:14-27        sg_results
+ *   InstrumentationCounters  dp.hpp:46-66           sg_results.counters
+ *   cigar_to_string          cigar.cpp:18-25        sg_cigar_string
+ *   write_batch_tsv          batch.cpp:106-113      sg_results + sg_cigar_string
+ *   encode_sequence          sequence.hpp:19-37     codes in sg_pairs (1 B/base)
+ *   InputError / ConfigError / InternalError        SG_INPUT / SG_CONFIG / SG_INTERNAL
+ *                            errors.hpp:10-34
+ *
+ * Semantics: identical edit distance and CIGAR to the reference for every
+ * pair at the same (W, O, sene, dent, early_termination). The switches only
+ * change work and footprint in the reference (proj/tests/acceptance.cpp:93-126);
+ * the GPU always runs early termination with a 2-bit-per-cell trimmed table
+ * and reports the reference's counters for the requested switches.
+ */
+#ifndef SCROOGE_B200_H
+#define SCROOGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+/* Status codes (proj/tools/main.cpp:287-299 maps the same classes to exit codes). */
+enum {
+    SG_OK = 0,
+    SG_INPUT = 1,    /* scrooge::InputError */
+    SG_CONFIG = 2,   /* scrooge::ConfigError */
+    SG_INTERNAL = 3, /* scrooge::InternalError (incl. OutOfStoredRegionError) */
+    SG_CUDA = 4      /* device / driver failure (no reference equivalent) */
+};
+
+/* AlignerConfig, proj/include/scrooge/aligner.hpp:12-31. Defaults W=64, O=33,
+ * all switches on (sg_config_default). single_window selects
+ * Mode::SingleWindow (not supported on the GPU path yet: SG_CONFIG). */
+typedef struct sg_config {
+    int32_t W;
+    int32_t O;
+    uint8_t sene;
+    uint8_t dent;
+    uint8_t early_termination;
+    uint8_t single_window;
+    int32_t k_single;
+} sg_config;
+
+/* Pairs as 1-byte base codes (proj/include/scrooge/sequence.hpp:13-16:
+ * 0..3 = A,C,G,T; anything else = non-ACGT, matches nothing).
+ * Sequence k of the batch is text[text_off[k] .. text_off[k] + text_len[k]). */
+typedef struct sg_pairs {
+    int64_t n_pairs;
+    const uint8_t* text;
+    const int64_t* text_off;
+    const int64_t* text_len;
+    const uint8_t* pattern;
+    const int64_t* pat_off;
+    const int64_t* pat_len;
+} sg_pairs;
+
+/* Pairs already 2-bit packed (BASELINE cfg2's input form): 16 bases per word,
+ * base k at bits 2(k%16)..2(k%16)+1 of word k/16 (A=0 C=1 G=2 T=3). Offsets
+ * are in bases. nmask (optional, NULL = pure ACGT) holds 1 bit per base at the
+ * same offsets (bit k%32 of word k/32); a set bit marks a non-ACGT base. */
+typedef struct sg_packed_pairs {
+    int64_t n_pairs;
+    const uint32_t* seq;
+    int64_t seq_words;
+    const uint32_t* nmask;
+    const int64_t* text_off;
+    const int64_t* text_len;
+    const int64_t* pat_off;
+    const int64_t* pat_len;
+} sg_packed_pairs;
+
+/* Run encoding of CIGARs: one byte per run piece, (op << 6) | (len - 1),
+ * op 0 '=', 1 'X', 2 'I', 3 'D', len 1..64. Consecutive bytes with the same
+ * op continue one run (cigar_append merges, proj/src/cigar.cpp:9-16, so two
+ * real runs never share an op). */
+enum { SG_OP_MATCH = 0, SG_OP_SUB = 1, SG_OP_INS = 2, SG_OP_DEL = 3 };
+
+/* Counter slots per pair, InstrumentationCounters order (dp.hpp:46-66). */
+enum {
+    SG_CNT_STORED_BITS = 0,
+    SG_CNT_TABLE_WRITES,
+    SG_CNT_TABLE_READS,
+    SG_CNT_ROWS_COMPUTED,
+    SG_CNT_CELLS_COMPUTED,
+    SG_CNT_ROWS_POSSIBLE,
+    SG_CNT_BASELINE_EQUIV_BITS,
+    SG_CNT_COUNT
+};
+
+/* PairOutcome / BatchResult, proj/include/scrooge/batch.hpp:14-27, in input order. */
+typedef struct sg_results {
+    int64_t n_pairs;
+    int64_t* distance;     /* [n] */
+    int32_t* windows;      /* [n] */
+    uint8_t* found;        /* [n] (always 1 in windowed mode) */
+    int64_t* cigar_off;    /* [n+1] byte offsets into runs */
+    uint8_t* runs;         /* run bytes, see SG_OP_* */
+    uint64_t* counters;    /* [n][SG_CNT_COUNT] */
+    uint64_t total[SG_CNT_COUNT]; /* BatchResult::total */
+    double align_seconds;  /* host wall time of the whole call (H2D + kernels + D2H) */
+    double device_ms;      /* device time of the kernels (CUDA events, max over devices) */
+    double kernel_ms;      /* device time of K1 alone (max over devices) */
+    int64_t gpu_launches;  /* kernels launched by this call */
+    void* _owner;          /* internal */
+} sg_results;
+
+/* Library info. */
+int sg_abi_version(void);
+int sg_device_count(void);
+const char* sg_last_error(void); /* message of the last failing call on this thread */
+
+void sg_config_default(sg_config* cfg);
+/* AlignerConfig::validate (aligner.cpp:8-18) + GPU-path limits. */
+int sg_validate_config(const sg_config* cfg);
+
+/* run_batch over 1-byte codes: validates, packs (host threads), shards the
+ * pairs over `devices` (NULL = device 0; n_devices >= 1), runs K1-K3, copies
+ * results back. Blocking. On SG_INPUT / SG_INTERNAL the message names the
+ * first failing pair by index ("pair '<index>': ..."), as batch.cpp:69-77. */
+int sg_align_batch(const sg_config* cfg, const sg_pairs* pairs, const int* devices,
+                   int n_devices, sg_results* out);
+/* Same over 2-bit packed input (no host packing). */
+int sg_align_packed(const sg_config* cfg, const sg_packed_pairs* pairs, const int* devices,
+                    int n_devices, sg_results* out);
+void sg_results_free(sg_results* res);
+
+/* cigar_to_string of pair k: writes "<len><op>..." + NUL into buf when it fits;
+ * returns the string length (excl. NUL), or -1 on a bad index. */
+int64_t sg_cigar_string(const sg_results* res, int64_t k, char* buf, int64_t cap);
+/* Decoded runs of pair k into ops[] ('=','X','I','D') / lens[]; returns the
+ * run count (may exceed cap: then only cap runs are written). */
+int64_t sg_cigar_runs(const sg_results* res, int64_t k, char* ops, int64_t* lens, int64_t cap);
+
+/* 2-bit packing (K4) of 1-byte codes with host threads. The packed buffers are
+ * owned by `out` and released with sg_packed_free. Each sequence starts on a
+ * word boundary. */
+int sg_pack(const sg_pairs* in, sg_packed_pairs* out);
+void sg_packed_free(sg_packed_pairs* p);
+
+/* Bytes copied host->device (direction 0) / device->host (1) by the last
+ * sg_align_batch / sg_align_packed call on this thread. */
+int64_t sg_last_transfer_bytes(int direction);
+
+/* Device-resident sessions (inputs already in HBM when timing starts). */
+typedef struct sg_session sg_session;
+int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int device,
+                      sg_session** out);
+/* Runs K1-K3 once on the session's stream; returns device ms (CUDA events). */
+int sg_session_run(sg_session* s, float* device_ms, float* k1_ms);
+int sg_session_fetch(sg_session* s, sg_results* out);
+/* Per-session facts for the roofline: resident lanes, SMs, K1 launches. */
+int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* limbs);
+void sg_session_destroy(sg_session* s);
+
+/* Seeded synthetic pairs of the BASELINE configs (paper_2208_09985_b200/csrc/
+ * synth.h), generated straight into packed form with host threads. */
+int sg_synth_packed(int cfg_id, int64_t first, int64_t count, sg_packed_pairs* out);
+/* Same pairs as 1-byte codes (buffers owned by out, free with sg_pairs_free). */
+int sg_synth_codes(int cfg_id, int64_t first, int64_t count, sg_pairs* out);
+void sg_pairs_free(sg_pairs* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCROOGE_B200_H */

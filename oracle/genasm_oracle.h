@@ -1,0 +1,69 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference's windowed GenASM aligner
+ * (/root/reference/proj/src/{aligner,dp,traceback,cigar}.cpp). Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load it, and only as the checker or the CPU baseline. The product path
+ * (paper_2208_09985_b200) never links or calls it.
+ *
+ * Parity pin: tests/test_oracle_pin.py checks this restatement against golden
+ * vectors produced by the reference itself (oracle/_ref/ref_tool, built from
+ * the reference sources by oracle/Makefile; fixtures in tests/golden/).
+ */
+#ifndef GENASM_ORACLE_H
+#define GENASM_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* proj/include/scrooge/aligner.hpp:12-31 */
+typedef struct orc_config {
+    int32_t W, O;
+    uint8_t sene, dent, et;
+    uint8_t single_window; /* Mode::SingleWindow */
+    int32_t k_single;
+} orc_config;
+
+/* proj/include/scrooge/dp.hpp:46-66 */
+typedef struct orc_counters {
+    uint64_t stored_bits, table_writes, table_reads, rows_computed, cells_computed,
+        rows_possible, baseline_equiv_bits;
+} orc_counters;
+
+typedef struct orc_result {
+    int32_t found;    /* 0 only in single-window mode past k */
+    int64_t distance; /* -1 when !found */
+    int32_t windows;
+    int64_t n_runs;
+    char* ops;        /* run ops '=', 'X', 'I', 'D' (malloc'ed) */
+    int64_t* lens;    /* run lengths (malloc'ed) */
+    orc_counters counters;
+} orc_result;
+
+enum { ORC_OK = 0, ORC_INPUT = 1, ORC_CONFIG = 2, ORC_INTERNAL = 3 };
+
+/* align() (proj/src/aligner.cpp:28-85) or align_single_window() (:87-112)
+ * depending on cfg->single_window. Codes 0..3 = ACGT, 4 = other. */
+int orc_align(const orc_config* cfg, const uint8_t* text, int64_t n, const uint8_t* pattern,
+              int64_t m, orc_result* out, char* err, size_t errlen);
+void orc_result_free(orc_result* r);
+
+/* cigar_to_string (proj/src/cigar.cpp:18-25); returns bytes written (excl. NUL),
+ * or the required size when buf is too small. */
+int64_t orc_cigar_string(const orc_result* r, char* buf, int64_t cap);
+
+/* Per-window statistics hook: d_opt and window geometry of every window of
+ * the last orc_align call on this thread (for ALG_OPS/design studies). */
+int64_t orc_last_window_count(void);
+void orc_last_window_stats(int32_t* d_opt, int32_t* n_w, int32_t* m_w, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

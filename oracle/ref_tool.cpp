@@ -1,0 +1,155 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// Drives the UNMODIFIED reference library (libscrooge_core.a compiled by
+// oracle/Makefile from /root/reference/proj/src into oracle/_ref/) through its
+// public API: scrooge::align / scrooge::run_batch (proj/include/scrooge/
+// aligner.hpp:45, batch.hpp:33-34). Used to (1) produce the golden vectors
+// that pin oracle/genasm_oracle.c and the GPU path, and (2) time the
+// reference CPU aligner for bench.py --impl reference / cpu_baseline.
+//
+//   ref_tool align  --input pairs.tsv [cfg flags] [--hash]   per-pair results
+//   ref_tool synth  --cfg N --first F --count C [cfg flags] [--hash]
+//   ref_tool bench  --cfg N --first F --count C --threads T [cfg flags]
+// cfg flags: --W w --O o --sene 0|1 --dent 0|1 --et 0|1 --mode windowed|single --k k
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "scrooge/batch.hpp"
+#include "scrooge/errors.hpp"
+#include "scrooge/io.hpp"
+#include "synth.h"
+
+namespace {
+
+struct Args {
+    std::string cmd, input;
+    int cfg = 1;
+    long long first = 0, count = -1;
+    int threads = 1;
+    bool hash = false;
+    scrooge::AlignerConfig config;
+};
+
+std::uint64_t fnv1a(const std::string& s) {
+    std::uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+    return h;
+}
+
+Args parse(int argc, char** argv) {
+    Args a;
+    if (argc < 2) throw scrooge::InputError("usage: ref_tool align|synth|bench ...");
+    a.cmd = argv[1];
+    for (int i = 2; i < argc; ++i) {
+        std::string k = argv[i];
+        auto val = [&]() -> std::string {
+            if (i + 1 >= argc) throw scrooge::InputError("missing value for " + k);
+            return argv[++i];
+        };
+        if (k == "--input") a.input = val();
+        else if (k == "--cfg") a.cfg = std::stoi(val());
+        else if (k == "--first") a.first = std::stoll(val());
+        else if (k == "--count") a.count = std::stoll(val());
+        else if (k == "--threads") a.threads = std::stoi(val());
+        else if (k == "--hash") a.hash = true;
+        else if (k == "--W") a.config.W = std::stoi(val());
+        else if (k == "--O") a.config.O = std::stoi(val());
+        else if (k == "--sene") a.config.sene = std::stoi(val()) != 0;
+        else if (k == "--dent") a.config.dent = std::stoi(val()) != 0;
+        else if (k == "--et") a.config.early_termination = std::stoi(val()) != 0;
+        else if (k == "--k") a.config.k_single = std::stoi(val());
+        else if (k == "--mode") {
+            const std::string m = val();
+            a.config.mode = m == "single" ? scrooge::AlignerConfig::Mode::SingleWindow
+                                          : scrooge::AlignerConfig::Mode::Windowed;
+        } else throw scrooge::InputError("unknown flag " + k);
+    }
+    return a;
+}
+
+std::vector<scrooge::SeqPairRecord> synth_pairs(const Args& a) {
+    sg_synth_spec spec;
+    if (!sg_synth_baseline_spec(a.cfg, &spec)) throw scrooge::InputError("bad --cfg");
+    const long long count = a.count < 0 ? spec.n_pairs - a.first : a.count;
+    std::vector<scrooge::SeqPairRecord> pairs(static_cast<std::size_t>(count));
+    const int nt = static_cast<int>(std::min<long long>(16, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            std::vector<std::uint8_t> tb(sg_synth_max_text(&spec)), pb(sg_synth_max_pattern(&spec));
+            for (long long q = t; q < count; q += nt) {
+                std::int64_t n = 0, m = 0;
+                sg_synth_pair(&spec, a.first + q, tb.data(), &n, pb.data(), &m);
+                auto& r = pairs[static_cast<std::size_t>(q)];
+                r.id = "p" + std::to_string(a.first + q);
+                r.text.resize(static_cast<std::size_t>(n));
+                r.pattern.resize(static_cast<std::size_t>(m));
+                for (std::int64_t i = 0; i < n; ++i) r.text[i] = "ACGT"[tb[i]];
+                for (std::int64_t i = 0; i < m; ++i) r.pattern[i] = "ACGT"[pb[i]];
+            }
+        });
+    for (auto& th : pool) th.join();
+    return pairs;
+}
+
+void print_results(const std::vector<scrooge::SeqPairRecord>& pairs, const scrooge::BatchResult& br,
+                   bool hash) {
+    for (std::size_t i = 0; i < pairs.size(); ++i) {
+        const auto& po = br.outcomes[i];
+        const std::string cig = po.found ? scrooge::cigar_to_string(po.cigar) : "*";
+        const auto& c = po.counters;
+        std::printf("%s\t%lld\t", pairs[i].id.c_str(), static_cast<long long>(po.distance));
+        if (hash)
+            std::printf("%016llx\t%zu", static_cast<unsigned long long>(fnv1a(cig)), po.cigar.size());
+        else
+            std::printf("%s", cig.c_str());
+        std::printf("\t%d\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\n", po.windows,
+                    (unsigned long long)c.stored_bits, (unsigned long long)c.table_writes,
+                    (unsigned long long)c.table_reads, (unsigned long long)c.rows_computed,
+                    (unsigned long long)c.cells_computed, (unsigned long long)c.rows_possible,
+                    (unsigned long long)c.baseline_equiv_bits);
+    }
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        const Args a = parse(argc, argv);
+        if (a.cmd == "align") {
+            const auto pairs = scrooge::read_pairs_tsv(a.input);
+            print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);
+        } else if (a.cmd == "synth") {
+            const auto pairs = synth_pairs(a);
+            print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);
+        } else if (a.cmd == "bench") {
+            const auto pairs = synth_pairs(a);
+            const scrooge::BatchResult br = scrooge::run_batch(pairs, a.config, a.threads);
+            std::uint64_t cells = 0, dsum = 0;
+            for (const auto& po : br.outcomes) {
+                cells += po.counters.cells_computed;
+                dsum += static_cast<std::uint64_t>(po.distance);
+            }
+            std::printf(
+                "{\"pairs\": %zu, \"threads\": %d, \"align_seconds\": %.6f, \"pairs_per_second\": "
+                "%.3f, \"cells_computed\": %llu, \"distance_sum\": %llu}\n",
+                pairs.size(), a.threads, br.align_seconds, br.pairs_per_second,
+                (unsigned long long)cells, (unsigned long long)dsum);
+        } else {
+            throw scrooge::InputError("unknown command " + a.cmd);
+        }
+    } catch (const scrooge::InternalError& e) {
+        std::fprintf(stderr, "internal error: %s\n", e.what());
+        return 2;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    return 0;
+}

@@ -1,0 +1,1191 @@
+// Host runtime behind the C ABI (include/scrooge_b200.h): validation,
+// 2-bit packing (K4), per-device pipelines (H2D -> K1 -> K2 -> K3 -> D2H),
+// static cost-balanced sharding over devices with one host thread each (K5),
+// device-resident sessions, synthetic batches and run decoding.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/scrooge_b200.h"
+#include "synth.h"
+#include "window_align.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+struct Fail {  // thrown inside the runtime, converted to a status at the ABI
+    int code;
+};
+
+#define SG_CUDA_CHECK(expr)                                                             \
+    do {                                                                                \
+        cudaError_t e__ = (expr);                                                       \
+        if (e__ != cudaSuccess) {                                                       \
+            set_error(SG_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e__), \
+                      __FILE__, __LINE__, #expr);                                       \
+            throw Fail{SG_CUDA};                                                        \
+        }                                                                               \
+    } while (0)
+
+int hw_threads() {
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? static_cast<int>(std::min(h, 64u)) : 8;
+}
+
+// f(lo, hi, thread_index) over [0, n) in contiguous chunks.
+template <class F>
+void parallel_for(int64_t n, F&& f, int64_t grain = 1024) {
+    int threads = hw_threads();
+    threads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(threads, n / grain)));
+    if (threads <= 1) {
+        f(int64_t{0}, n, 0);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const int64_t chunk = (n + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+        const int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back([&f, lo, hi, t] { f(lo, hi, t); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+// ------------------------------------------------------------ pinned host memory
+
+// Grow-only pool so repeated calls do not re-pin memory inside timed regions.
+// Without a device (host-only helpers such as sg_pack / sg_synth_* on a CPU
+// box) it hands out pageable memory; computing still requires the GPU.
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> free_list;
+    std::vector<void*> pageable;  // blocks from malloc (never pinned)
+
+    void* acquire(size_t bytes, size_t* got) {
+        bytes = std::max<size_t>(bytes, 256);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            size_t bi = SIZE_MAX;
+            for (size_t k = 0; k < free_list.size(); ++k) {
+                const size_t c = free_list[k].second;
+                if (c >= bytes && c <= 2 * bytes + (size_t{64} << 20) &&
+                    (bi == SIZE_MAX || c < free_list[bi].second))
+                    bi = k;
+            }
+            if (bi != SIZE_MAX) {
+                void* p = free_list[bi].first;
+                *got = free_list[bi].second;
+                free_list.erase(free_list.begin() + static_cast<long>(bi));
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            p = std::malloc(bytes);
+            if (!p) {
+                set_error(SG_INTERNAL, "out of host memory (%zu bytes)", bytes);
+                throw Fail{SG_INTERNAL};
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            pageable.push_back(p);
+        }
+        *got = bytes;
+        return p;
+    }
+    void release(void* p, size_t bytes) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        free_list.emplace_back(p, bytes);
+    }
+};
+
+PinnedPool& pinned() {
+    static PinnedPool* pool = new PinnedPool();  // process lifetime
+    return *pool;
+}
+
+struct PinBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    void ensure(size_t bytes) {
+        if (p && bytes <= cap) return;
+        reset();
+        p = pinned().acquire(bytes, &cap);
+    }
+    void reset() {
+        if (p) pinned().release(p, cap);
+        p = nullptr;
+        cap = 0;
+    }
+    ~PinBuf() { reset(); }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// ------------------------------------------------------------ device memory
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        if (p && bytes <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        SG_CUDA_CHECK(cudaMalloc(&p, bytes));
+        cap = bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Device buffers, stream and events of one pipeline on one device.
+struct DevState {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[3] = {};
+    DevBuf seq, nmask, text_off, pat_off, text_len, pat_len, has_n, order;
+    DevBuf distance, windows, status, out_bytes, counters, bound_off, scratch, bnd, next_pair;
+    DevBuf dense_off, dense, scan_tmp;
+    long long grid = 0, lanes = 0;
+
+    void init(int dev) {
+        device = dev;
+        SG_CUDA_CHECK(cudaSetDevice(dev));
+        SG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SG_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        for (auto& e : ev) SG_CUDA_CHECK(cudaEventCreate(&e));
+    }
+    ~DevState() {
+        if (!stream) return;
+        cudaSetDevice(device);
+        for (DevBuf* b : {&seq, &nmask, &text_off, &pat_off, &text_len, &pat_len, &has_n, &order,
+                          &distance, &windows, &status, &out_bytes, &counters, &bound_off,
+                          &scratch, &bnd, &next_pair, &dense_off, &dense, &scan_tmp})
+            b->release();
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        cudaStreamDestroy(stream);
+    }
+};
+
+// One cached pipeline per device for the one-shot calls (serialised per device).
+struct DevSlot {
+    std::mutex mu;
+    std::unique_ptr<DevState> st;
+};
+// Intentionally leaked: no device teardown races the CUDA runtime at exit.
+std::mutex g_slots_mu;
+std::vector<DevSlot*>* g_slots = new std::vector<DevSlot*>();
+
+DevSlot& dev_slot(int dev) {
+    std::lock_guard<std::mutex> lk(g_slots_mu);
+    while (static_cast<int>(g_slots->size()) <= dev) g_slots->push_back(new DevSlot());
+    return *(*g_slots)[static_cast<size_t>(dev)];
+}
+
+// ------------------------------------------------------------ validation
+
+int limbs_for(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 0; }
+
+int validate_cfg(const sg_config* c) {
+    if (!c) return set_error(SG_CONFIG, "null config");
+    // AlignerConfig::validate, proj/src/aligner.cpp:8-18
+    if (c->W < 1 || c->W > 1024)
+        return set_error(SG_CONFIG, "window size W out of range: %d", c->W);
+    if (c->O < 0 || c->O >= c->W)
+        return set_error(SG_CONFIG, "window overlap O must satisfy 0 <= O < W, got O=%d W=%d",
+                         c->O, c->W);
+    if (c->dent && c->single_window)
+        return set_error(SG_CONFIG,
+                         "trimmed table storage cannot back a full single-window traceback");
+    if (c->single_window && (c->k_single < 0 || c->k_single > 1024))
+        return set_error(SG_CONFIG, "k out of range: %d", c->k_single);
+    // GPU-path limits (SURVEY §8(b) semantic gaps)
+    if (c->single_window)
+        return set_error(SG_CONFIG, "single-window mode is not implemented on the GPU path");
+    if (!limbs_for(c->W))
+        return set_error(SG_CONFIG, "the GPU path supports W <= 128, got W=%d", c->W);
+    return SG_OK;
+}
+
+int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl) {
+    for (int64_t k = 0; k < n; ++k) {
+        if (tl[k] <= 0 || pl[k] <= 0)  // batch.cpp:18-25
+            return set_error(SG_INPUT, "pair '%lld': empty sequence", static_cast<long long>(k));
+        if (tl[k] + pl[k] > (int64_t{1} << 30))
+            return set_error(SG_INPUT, "pair '%lld': sequence too long for one GPU pair slot",
+                             static_cast<long long>(k));
+    }
+    return SG_OK;
+}
+
+// ------------------------------------------------------------ packing (K4)
+
+// Owned packed batch (pinned, so it can be uploaded at full PCIe rate).
+struct Packed {
+    PinBuf seq, nmask, text_off, text_len, pat_off, pat_len;
+    int64_t n_pairs = 0, seq_words = 0;
+    bool any_n = false;
+    sg_packed_pairs view() const {
+        sg_packed_pairs v{};
+        v.n_pairs = n_pairs;
+        v.seq = seq.as<uint32_t>();
+        v.seq_words = seq_words;
+        v.nmask = any_n ? nmask.as<uint32_t>() : nullptr;
+        v.text_off = text_off.as<int64_t>();
+        v.text_len = text_len.as<int64_t>();
+        v.pat_off = pat_off.as<int64_t>();
+        v.pat_len = pat_len.as<int64_t>();
+        return v;
+    }
+};
+
+std::mutex g_owned_mu;
+std::vector<Packed*>& packed_registry() {
+    static auto* r = new std::vector<Packed*>();
+    return *r;
+}
+
+// Pack one sequence of 1-byte codes into 16-base words; returns true if it
+// holds a non-ACGT code (then nm, if given, receives its bits).
+bool pack_seq(const uint8_t* src, int64_t len, uint32_t* dst, uint32_t* nm, int64_t base) {
+    const int64_t words = (len + 15) / 16;
+    bool n = false;
+    int64_t k = 0;
+    for (int64_t w = 0; w < words; ++w) {
+        uint32_t v = 0;
+        const int64_t hi = std::min(len, k + 16);
+        for (int sh = 0; k < hi; ++k, sh += 2) {
+            const uint32_t c = src[k];
+            n |= c >= 4;
+            v |= (c & 3u) << sh;
+        }
+        dst[w] = v;
+    }
+    if (n && nm)
+        for (int64_t i = 0; i < len; ++i)
+            if (src[i] >= 4) {
+                const int64_t b = base + i;
+                __atomic_fetch_or(&nm[b >> 5], 1u << (b & 31), __ATOMIC_RELAXED);
+            }
+    return n;
+}
+
+void layout_offsets(Packed& pk, int64_t n, const int64_t* tl, const int64_t* pl) {
+    pk.n_pairs = n;
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    pk.text_off.ensure(8 * n1);
+    pk.text_len.ensure(8 * n1);
+    pk.pat_off.ensure(8 * n1);
+    pk.pat_len.ensure(8 * n1);
+    int64_t words = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        pk.text_off.as<int64_t>()[k] = words * 16;
+        pk.text_len.as<int64_t>()[k] = tl[k];
+        words += (tl[k] + 15) / 16;
+        pk.pat_off.as<int64_t>()[k] = words * 16;
+        pk.pat_len.as<int64_t>()[k] = pl[k];
+        words += (pl[k] + 15) / 16;
+    }
+    pk.seq_words = words;
+    pk.seq.ensure(4 * static_cast<size_t>(words + 1));
+    pk.seq.as<uint32_t>()[words] = 0;
+}
+
+void pack_pairs(const sg_pairs* in, Packed& pk) {
+    const int64_t n = in->n_pairs;
+    layout_offsets(pk, n, in->text_len, in->pat_len);
+    std::atomic<bool> any{false};
+    parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+        bool a = false;
+        for (int64_t k = lo; k < hi && !a; ++k) {
+            const uint8_t* t = in->text + in->text_off[k];
+            const uint8_t* p = in->pattern + in->pat_off[k];
+            for (int64_t i = 0; i < in->text_len[k] && !a; ++i) a = t[i] >= 4;
+            for (int64_t i = 0; i < in->pat_len[k] && !a; ++i) a = p[i] >= 4;
+        }
+        if (a) any = true;
+    });
+    pk.any_n = any.load();
+    uint32_t* nm = nullptr;
+    if (pk.any_n) {
+        const size_t nm_words = static_cast<size_t>((pk.seq_words * 16 + 31) / 32 + 2);
+        pk.nmask.ensure(4 * nm_words);
+        nm = pk.nmask.as<uint32_t>();
+        std::memset(nm, 0, 4 * nm_words);
+    }
+    uint32_t* seq = pk.seq.as<uint32_t>();
+    parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+        for (int64_t k = lo; k < hi; ++k) {
+            const int64_t to = pk.text_off.as<int64_t>()[k], po = pk.pat_off.as<int64_t>()[k];
+            pack_seq(in->text + in->text_off[k], in->text_len[k], seq + to / 16, nm, to);
+            pack_seq(in->pattern + in->pat_off[k], in->pat_len[k], seq + po / 16, nm, po);
+        }
+    });
+}
+
+// ------------------------------------------------------------ results
+
+struct ResultOwner {
+    PinBuf distance, windows, found, cigar_off, runs, counters;
+};
+
+void results_alloc(sg_results* out, int64_t n, int64_t run_bytes) {
+    auto own = std::make_unique<ResultOwner>();
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    own->distance.ensure(8 * n1);
+    own->windows.ensure(4 * n1);
+    own->found.ensure(n1);
+    own->cigar_off.ensure(8 * (n1 + 1));
+    own->runs.ensure(static_cast<size_t>(std::max<int64_t>(run_bytes, 1)));
+    own->counters.ensure(8 * SG_CNT_COUNT * n1);
+    std::memset(out, 0, sizeof *out);
+    out->n_pairs = n;
+    out->distance = own->distance.as<int64_t>();
+    out->windows = own->windows.as<int32_t>();
+    out->found = own->found.as<uint8_t>();
+    out->cigar_off = own->cigar_off.as<int64_t>();
+    out->runs = own->runs.as<uint8_t>();
+    out->counters = own->counters.as<uint64_t>();
+    out->cigar_off[0] = 0;
+    out->_owner = own.release();
+}
+
+// ------------------------------------------------------------ one shard
+
+struct Shard {
+    const sg_packed_pairs* in;
+    int64_t lo, hi;
+};
+
+// Host-side per-pair inputs of a shard: rebased offsets, lengths, bounds, order.
+struct ShardPrep {
+    PinBuf text_off, pat_off, text_len, pat_len, has_n, bound_off, order;
+    int64_t n = 0;
+    int64_t word_lo = 0, word_hi = 0;
+    int64_t scratch_bytes = 0;
+    bool any_n = false;
+    bool ordered = false;
+};
+
+bool any_bits(const uint32_t* m, int64_t base, int64_t len) {
+    for (int64_t k = 0; k < len; ++k) {
+        const int64_t b = base + k;
+        if ((m[b >> 5] >> (b & 31)) & 1u) return true;
+    }
+    return false;
+}
+
+void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first) {
+    const sg_packed_pairs* in = s.in;
+    const int64_t n = s.hi - s.lo;
+    pp.n = n;
+    int64_t wlo = INT64_MAX, whi = 0;
+    for (int64_t k = s.lo; k < s.hi; ++k) {
+        wlo = std::min({wlo, in->text_off[k] >> 4, in->pat_off[k] >> 4});
+        whi = std::max({whi, (in->text_off[k] + in->text_len[k] + 15) >> 4,
+                        (in->pat_off[k] + in->pat_len[k] + 15) >> 4});
+    }
+    if (n == 0) wlo = whi = 0;
+    wlo &= ~int64_t{1};  // even word: the N mask stays 32-bit aligned after rebasing
+    pp.word_lo = wlo;
+    pp.word_hi = whi;
+    const int64_t rebase = wlo * 16;
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    pp.text_off.ensure(8 * n1);
+    pp.pat_off.ensure(8 * n1);
+    pp.text_len.ensure(4 * n1);
+    pp.pat_len.ensure(4 * n1);
+    pp.has_n.ensure(n1);
+    pp.bound_off.ensure(8 * n1);
+    int64_t bound = 0;
+    bool any_n = false;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t g = s.lo + k;
+        pp.text_off.as<int64_t>()[k] = in->text_off[g] - rebase;
+        pp.pat_off.as<int64_t>()[k] = in->pat_off[g] - rebase;
+        pp.text_len.as<int32_t>()[k] = static_cast<int32_t>(in->text_len[g]);
+        pp.pat_len.as<int32_t>()[k] = static_cast<int32_t>(in->pat_len[g]);
+        bool hn = false;
+        if (in->nmask)
+            hn = any_bits(in->nmask, in->text_off[g], in->text_len[g]) ||
+                 any_bits(in->nmask, in->pat_off[g], in->pat_len[g]);
+        pp.has_n.as<uint8_t>()[k] = hn;
+        any_n |= hn;
+        pp.bound_off.as<int64_t>()[k] = bound;
+        // at most one run byte per edit op, ops <= n + m
+        bound += ((in->text_len[g] + in->pat_len[g] + 3) & ~int64_t{3}) + 4;
+    }
+    pp.any_n = any_n;
+    pp.scratch_bytes = bound;
+    pp.ordered = longest_first && n > 1;
+    if (pp.ordered) {
+        pp.order.ensure(4 * static_cast<size_t>(n));
+        int32_t* o = pp.order.as<int32_t>();
+        std::iota(o, o + n, 0);
+        std::stable_sort(o, o + n, [&](int32_t a, int32_t b) {
+            return in->text_len[s.lo + a] + in->pat_len[s.lo + a] >
+                   in->text_len[s.lo + b] + in->pat_len[s.lo + b];
+        });
+    }
+}
+
+struct RunConfig {
+    int L, W, O, et, policy;
+};
+
+RunConfig run_config(const sg_config* c) {
+    RunConfig r;
+    r.L = limbs_for(c->W);
+    r.W = c->W;
+    r.O = c->O;
+    r.et = c->early_termination ? 1 : 0;
+    r.policy = c->dent ? 2 : c->sene ? 1 : 0;
+    return r;
+}
+
+int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp) {
+    const int64_t n = pp.n;
+    const sg_packed_pairs* in = s.in;
+    const int64_t words = pp.word_hi - pp.word_lo;
+    int64_t h2d_bytes = 0;
+    const size_t seq_bytes = 4 * static_cast<size_t>(words + 8);
+    st.seq.ensure(seq_bytes);
+    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 8, in->seq_words - pp.word_lo));
+    if (avail > 0) {
+        SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.p, in->seq + pp.word_lo, 4 * static_cast<size_t>(avail),
+                                      cudaMemcpyHostToDevice, st.stream));
+        h2d_bytes += 4 * avail;
+    }
+    if (static_cast<size_t>(4 * avail) < seq_bytes)
+        SG_CUDA_CHECK(cudaMemsetAsync(static_cast<char*>(st.seq.p) + 4 * avail, 0,
+                                      seq_bytes - 4 * static_cast<size_t>(avail), st.stream));
+    if (pp.any_n) {
+        const int64_t mlo = pp.word_lo / 2;
+        const int64_t mwords = (words + 1) / 2 + 4;
+        const int64_t mtot = (in->seq_words * 16 + 31) / 32;
+        st.nmask.ensure(4 * static_cast<size_t>(mwords));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.nmask.p, 0, 4 * static_cast<size_t>(mwords), st.stream));
+        const int64_t ma = std::min<int64_t>(mwords, mtot - mlo);
+        if (ma > 0) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(st.nmask.p, in->nmask + mlo, 4 * static_cast<size_t>(ma),
+                                          cudaMemcpyHostToDevice, st.stream));
+            h2d_bytes += 4 * ma;
+        }
+    }
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    auto h2d = [&](DevBuf& d, const PinBuf& h, size_t elem) {
+        d.ensure(elem * n1);
+        if (n) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(d.p, h.p, elem * static_cast<size_t>(n),
+                                          cudaMemcpyHostToDevice, st.stream));
+            h2d_bytes += static_cast<int64_t>(elem) * n;
+        }
+    };
+    h2d(st.text_off, pp.text_off, 8);
+    h2d(st.pat_off, pp.pat_off, 8);
+    h2d(st.text_len, pp.text_len, 4);
+    h2d(st.pat_len, pp.pat_len, 4);
+    h2d(st.has_n, pp.has_n, 1);
+    h2d(st.bound_off, pp.bound_off, 8);
+    if (pp.ordered) h2d(st.order, pp.order, 4);
+    return h2d_bytes;
+}
+
+// Sizes the per-run buffers and launches K1, K2 (3 kernels) and K3.
+// Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
+int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
+    const int64_t n = pp.n;
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    st.distance.ensure(4 * n1);
+    st.windows.ensure(4 * n1);
+    st.status.ensure(4 * n1);
+    st.out_bytes.ensure(4 * n1);
+    st.counters.ensure(8 * SG_CNT_COUNT * n1);
+    st.scratch.ensure(static_cast<size_t>(pp.scratch_bytes));
+    st.next_pair.ensure(64);
+    st.dense_off.ensure(8 * (n1 + 1));
+    st.dense.ensure(static_cast<size_t>(pp.scratch_bytes));
+    st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
+    int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    const int wpb = sgk::k1_warps_per_block(rc.L);
+    long long grid = static_cast<long long>(st.sms) * blocks_per_sm;
+    const long long need = (n + 32LL * wpb - 1) / (32LL * wpb);
+    grid = std::max(1LL, std::min(grid, need));
+    st.grid = grid;
+    st.lanes = grid * wpb * 32;
+    st.bnd.ensure(sgk::bnd_scratch_bytes(rc.L, grid * wpb));
+    SG_CUDA_CHECK(cudaMemsetAsync(st.next_pair.p, 0, 4, st.stream));
+
+    sgk::AlignParams p{};
+    p.seq = st.seq.as<uint32_t>();
+    p.nmask = pp.any_n ? st.nmask.as<uint32_t>() : nullptr;
+    p.text_off = st.text_off.as<int64_t>();
+    p.pat_off = st.pat_off.as<int64_t>();
+    p.text_len = st.text_len.as<int32_t>();
+    p.pat_len = st.pat_len.as<int32_t>();
+    p.has_n = pp.any_n ? st.has_n.as<uint8_t>() : nullptr;
+    p.order = pp.ordered ? st.order.as<int32_t>() : nullptr;
+    p.n_pairs = static_cast<int32_t>(n);
+    p.W = rc.W;
+    p.O = rc.O;
+    p.et = rc.et;
+    p.policy = rc.policy;
+    p.distance = st.distance.as<int32_t>();
+    p.windows = st.windows.as<int32_t>();
+    p.status = st.status.as<int32_t>();
+    p.out_bytes = st.out_bytes.as<int32_t>();
+    p.counters = st.counters.as<uint64_t>();
+    p.bound_off = st.bound_off.as<int64_t>();
+    p.scratch = st.scratch.as<uint32_t>();
+    p.bnd = st.bnd.as<uint32_t>();
+    p.next_pair = st.next_pair.as<unsigned int>();
+
+    int launches = 0;
+    SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
+    if (n > 0) {
+        SG_CUDA_CHECK(static_cast<cudaError_t>(
+            sgk::launch_window_align(rc.L, p, static_cast<int>(grid), wpb, st.stream)));
+        ++launches;
+    }
+    SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
+    SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_offsets(
+        st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), static_cast<int32_t>(n),
+        st.scan_tmp.p, st.scan_tmp.cap, st.stream)));
+    launches += n > 0 ? 3 : 0;
+    SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_compact(
+        st.scratch.as<uint32_t>(), st.bound_off.as<int64_t>(), st.dense_off.as<int64_t>(),
+        st.out_bytes.as<int32_t>(), st.dense.as<uint8_t>(), static_cast<int32_t>(n), st.stream)));
+    launches += n > 0 ? 1 : 0;
+    SG_CUDA_CHECK(cudaEventRecord(st.ev[2], st.stream));
+    return launches;
+}
+
+// Small per-pair outputs of a shard, staged in pinned memory.
+struct ShardOut {
+    PinBuf dist, win, status, doff, cnt;
+    int64_t run_bytes = 0;
+    float device_ms = 0, k1_ms = 0;
+    int launches = 0;
+    int err = SG_OK;
+    std::string msg;
+    int64_t first_bad = -1;
+    int32_t first_bad_status = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
+};
+
+void fetch_small(DevState& st, int64_t n, ShardOut& so) {
+    const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+    so.dist.ensure(4 * n1);
+    so.win.ensure(4 * n1);
+    so.status.ensure(4 * n1);
+    so.doff.ensure(8 * (n1 + 1));
+    so.cnt.ensure(8 * SG_CNT_COUNT * n1);
+    auto d2h = [&](PinBuf& h, const DevBuf& d, size_t bytes) {
+        if (bytes) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(h.p, d.p, bytes, cudaMemcpyDeviceToHost, st.stream));
+            so.d2h_bytes += static_cast<int64_t>(bytes);
+        }
+    };
+    const size_t un = static_cast<size_t>(n);
+    d2h(so.dist, st.distance, 4 * un);
+    d2h(so.win, st.windows, 4 * un);
+    d2h(so.status, st.status, 4 * un);
+    d2h(so.doff, st.dense_off, 8 * (un + 1));
+    d2h(so.cnt, st.counters, 8 * SG_CNT_COUNT * un);
+    SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+    so.run_bytes = so.doff.as<int64_t>()[n];
+    for (int64_t k = 0; k < n; ++k)
+        if (so.status.as<int32_t>()[k] != 0) {
+            so.first_bad = k;
+            so.first_bad_status = so.status.as<int32_t>()[k];
+            break;
+        }
+    float ms = 0, k1 = 0;
+    SG_CUDA_CHECK(cudaEventElapsedTime(&ms, st.ev[0], st.ev[2]));
+    SG_CUDA_CHECK(cudaEventElapsedTime(&k1, st.ev[0], st.ev[1]));
+    so.device_ms = ms;
+    so.k1_ms = k1;
+}
+
+const char* status_detail(int32_t s) {
+    switch (s & ~0xFFFF) {
+        case sgk::kDetBudgetI: return "traceback: budget != remaining pattern";
+        case sgk::kDetBudgetD: return "traceback: budget != remaining text";
+        case sgk::kDetLeftover: return "traceback: finished with leftover budget";
+        case sgk::kDetWatchdog: return "windowed alignment: window count exceeded watchdog cap";
+        case sgk::kDetNoStep: return "traceback: no legal step";
+        case sgk::kDetSegment: return "window continuation disagrees with the traceback budget";
+        default: return "internal error";
+    }
+}
+
+// Copies a shard's small outputs into the public result at pair `base`.
+void scatter_small(sg_results* out, int64_t base, int64_t n, int64_t run_base, const ShardOut& so) {
+    const int32_t* dist = so.dist.as<int32_t>();
+    const int32_t* win = so.win.as<int32_t>();
+    const int64_t* doff = so.doff.as<int64_t>();
+    for (int64_t k = 0; k < n; ++k) {
+        out->distance[base + k] = dist[k];
+        out->windows[base + k] = win[k];
+        out->found[base + k] = 1;
+        out->cigar_off[base + k] = run_base + doff[k];
+    }
+    out->cigar_off[base + n] = run_base + doff[n];
+    if (n)
+        std::memcpy(out->counters + base * SG_CNT_COUNT, so.cnt.p,
+                    8 * SG_CNT_COUNT * static_cast<size_t>(n));
+}
+
+void finish_totals(sg_results* out) {
+    for (int c = 0; c < SG_CNT_COUNT; ++c) out->total[c] = 0;
+    for (int64_t k = 0; k < out->n_pairs; ++k)
+        for (int c = 0; c < SG_CNT_COUNT; ++c) out->total[c] += out->counters[k * SG_CNT_COUNT + c];
+}
+
+// ------------------------------------------------------------ batch driver
+
+thread_local int64_t g_last_h2d = 0, g_last_d2h = 0;
+
+int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int* devices,
+                      int n_devices, sg_results* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::memset(out, 0, sizeof *out);
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (!in || in->n_pairs < 0) return set_error(SG_INPUT, "null or negative pair batch");
+    const int64_t n = in->n_pairs;
+    if (n > INT32_MAX) return set_error(SG_INPUT, "too many pairs in one batch");
+    rc = validate_lengths(n, in->text_len, in->pat_len);
+    if (rc) return rc;
+    int dev_default = 0;
+    if (!devices || n_devices < 1) {
+        devices = &dev_default;
+        n_devices = 1;
+    }
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1)
+        return set_error(SG_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    for (int d = 0; d < n_devices; ++d)
+        if (devices[d] < 0 || devices[d] >= count)
+            return set_error(SG_CONFIG, "bad device index %d", devices[d]);
+    const RunConfig rcfg = run_config(cfg);
+    const size_t nd = static_cast<size_t>(n_devices);
+
+    // K5: contiguous shards with balanced cost (text + pattern length)
+    std::vector<int64_t> cut(nd + 1, 0);
+    {
+        int64_t total = 0;
+        for (int64_t k = 0; k < n; ++k) total += in->text_len[k] + in->pat_len[k];
+        int64_t acc = 0;
+        size_t d = 1;
+        for (int64_t k = 0; k < n && d < nd; ++k) {
+            acc += in->text_len[k] + in->pat_len[k];
+            while (d < nd && acc * static_cast<int64_t>(nd) >= total * static_cast<int64_t>(d))
+                cut[d++] = k + 1;
+        }
+        while (d < nd) cut[d++] = n;
+        cut[nd] = n;
+    }
+    bool mixed = false;
+    for (int64_t k = 1; k < n && !mixed; ++k)
+        mixed = in->text_len[k] + in->pat_len[k] != in->text_len[0] + in->pat_len[0];
+
+    std::vector<ShardOut> so(nd);
+    std::vector<ShardPrep> prep(nd);
+    std::vector<std::unique_lock<std::mutex>> locks(nd);
+    std::vector<DevState*> states(nd, nullptr);
+
+    auto run_phase = [&](auto&& body) {
+        if (nd == 1) {
+            body(0);
+            return;
+        }
+        std::vector<std::thread> th;
+        for (size_t d = 0; d < nd; ++d) th.emplace_back(body, d);
+        for (auto& t : th) t.join();
+    };
+    // phase 1: prep, upload, kernels, small D2H
+    run_phase([&](size_t d) {
+        ShardOut& o = so[d];
+        try {
+            SG_CUDA_CHECK(cudaSetDevice(devices[d]));
+            DevSlot& slot = dev_slot(devices[d]);
+            locks[d] = std::unique_lock<std::mutex>(slot.mu);
+            if (!slot.st) {
+                slot.st = std::make_unique<DevState>();
+                slot.st->init(devices[d]);
+            }
+            DevState& st = *slot.st;
+            states[d] = &st;
+            const Shard s{in, cut[d], cut[d + 1]};
+            prep_shard(s, prep[d], mixed);
+            o.h2d_bytes = upload_shard(st, s, prep[d]);
+            o.launches = launch_shard(st, rcfg, prep[d]);
+            fetch_small(st, prep[d].n, o);
+        } catch (const Fail& f) {
+            o.err = f.code;
+            o.msg = g_last_error;
+        }
+    });
+    for (auto& o : so)
+        if (o.err) return set_error(o.err, "%s", o.msg.c_str());
+    for (size_t d = 0; d < nd; ++d)  // first failing pair in input order (batch.cpp:94-97)
+        if (so[d].first_bad >= 0)
+            return set_error(SG_INTERNAL, "pair '%lld': %s",
+                             static_cast<long long>(cut[d] + so[d].first_bad),
+                             status_detail(so[d].first_bad_status));
+    int64_t run_total = 0;
+    std::vector<int64_t> run_base(nd);
+    for (size_t d = 0; d < nd; ++d) {
+        run_base[d] = run_total;
+        run_total += so[d].run_bytes;
+    }
+    try {
+        results_alloc(out, n, run_total);
+    } catch (const Fail& f) {
+        return f.code;
+    }
+    // phase 2: run bytes straight into the result buffer
+    run_phase([&](size_t d) {
+        ShardOut& o = so[d];
+        try {
+            SG_CUDA_CHECK(cudaSetDevice(devices[d]));
+            DevState& st = *states[d];
+            if (o.run_bytes) {
+                SG_CUDA_CHECK(cudaMemcpyAsync(out->runs + run_base[d], st.dense.p,
+                                              static_cast<size_t>(o.run_bytes),
+                                              cudaMemcpyDeviceToHost, st.stream));
+                o.d2h_bytes += o.run_bytes;
+            }
+            scatter_small(out, cut[d], cut[d + 1] - cut[d], run_base[d], o);
+            SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+        } catch (const Fail& f) {
+            o.err = f.code;
+            o.msg = g_last_error;
+        }
+        locks[d].unlock();
+    });
+    for (auto& o : so)
+        if (o.err) {
+            sg_results_free(out);
+            return set_error(o.err, "%s", o.msg.c_str());
+        }
+    finish_totals(out);
+    g_last_h2d = g_last_d2h = 0;
+    for (auto& o : so) {
+        out->device_ms = std::max(out->device_ms, static_cast<double>(o.device_ms));
+        out->kernel_ms = std::max(out->kernel_ms, static_cast<double>(o.k1_ms));
+        out->gpu_launches += o.launches;
+        g_last_h2d += o.h2d_bytes;
+        g_last_d2h += o.d2h_bytes;
+    }
+    out->align_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return SG_OK;
+}
+
+// ------------------------------------------------------------ synthetic batches
+
+// Generates pairs [first, first+count) of a BASELINE config in parallel.
+// emit(k, text, n, pattern, m) is called once per pair, from worker threads.
+template <class Emit>
+int synth_each(const sg_synth_spec& spec, int64_t first, int64_t count, Emit&& emit) {
+    std::atomic<int> bad{0};
+    parallel_for(count, [&](int64_t lo, int64_t hi, int) {
+        std::vector<uint8_t> tb(static_cast<size_t>(sg_synth_max_text(&spec)));
+        std::vector<uint8_t> pb(static_cast<size_t>(sg_synth_max_pattern(&spec)));
+        for (int64_t k = lo; k < hi; ++k) {
+            int64_t n = 0, m = 0;
+            if (sg_synth_pair(&spec, first + k, tb.data(), &n, pb.data(), &m)) {
+                bad = 1;
+                return;
+            }
+            emit(k, tb.data(), n, pb.data(), m);
+        }
+    }, 256);
+    return bad.load() ? set_error(SG_INPUT, "bad synthetic spec") : SG_OK;
+}
+
+struct OwnedCodes {
+    std::vector<uint8_t> text, pattern;
+    std::vector<int64_t> text_off, text_len, pat_off, pat_len;
+};
+std::mutex g_codes_mu;
+std::vector<OwnedCodes*>& codes_registry() {
+    static auto* r = new std::vector<OwnedCodes*>();
+    return *r;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+struct sg_session {
+    sg_config cfg;
+    RunConfig rc;
+    DevState st;
+    ShardPrep prep;
+    int64_t n = 0;
+    int launches = 0;
+    bool ran = false;
+};
+
+extern "C" {
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+
+int sg_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+const char* sg_last_error(void) { return g_last_error.c_str(); }
+
+void sg_config_default(sg_config* cfg) {
+    cfg->W = 64;
+    cfg->O = 33;
+    cfg->sene = 1;
+    cfg->dent = 1;
+    cfg->early_termination = 1;
+    cfg->single_window = 0;
+    cfg->k_single = 1024;
+}
+
+int sg_validate_config(const sg_config* cfg) { return validate_cfg(cfg); }
+
+int sg_align_packed(const sg_config* cfg, const sg_packed_pairs* pairs, const int* devices,
+                    int n_devices, sg_results* out) {
+    try {
+        return align_packed_impl(cfg, pairs, devices, n_devices, out);
+    } catch (const Fail& f) {
+        return f.code;
+    } catch (const std::exception& e) {
+        return set_error(SG_INTERNAL, "%s", e.what());
+    }
+}
+
+int sg_align_batch(const sg_config* cfg, const sg_pairs* pairs, const int* devices,
+                   int n_devices, sg_results* out) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::memset(out, 0, sizeof *out);
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (!pairs || pairs->n_pairs < 0) return set_error(SG_INPUT, "null or negative pair batch");
+    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len);
+    if (rc) return rc;
+    try {
+        Packed pk;
+        pack_pairs(pairs, pk);
+        const sg_packed_pairs v = pk.view();
+        rc = align_packed_impl(cfg, &v, devices, n_devices, out);
+    } catch (const Fail& f) {
+        return f.code;
+    } catch (const std::exception& e) {
+        return set_error(SG_INTERNAL, "%s", e.what());
+    }
+    if (rc == SG_OK)
+        out->align_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+void sg_results_free(sg_results* res) {
+    if (!res) return;
+    delete static_cast<ResultOwner*>(res->_owner);
+    std::memset(res, 0, sizeof *res);
+}
+
+int64_t sg_cigar_runs(const sg_results* res, int64_t k, char* ops, int64_t* lens, int64_t cap) {
+    if (!res || k < 0 || k >= res->n_pairs) return -1;
+    static const char kOp[4] = {'=', 'X', 'I', 'D'};
+    int64_t nr = 0;
+    int prev = -1;
+    for (int64_t b = res->cigar_off[k]; b < res->cigar_off[k + 1]; ++b) {
+        const uint8_t v = res->runs[b];
+        const int op = v >> 6;
+        const int64_t len = (v & 63) + 1;
+        if (op == prev) {
+            if (nr - 1 < cap) lens[nr - 1] += len;
+        } else {
+            if (nr < cap) {
+                ops[nr] = kOp[op];
+                lens[nr] = len;
+            }
+            ++nr;
+            prev = op;
+        }
+    }
+    return nr;
+}
+
+int64_t sg_cigar_string(const sg_results* res, int64_t k, char* buf, int64_t cap) {
+    if (!res || k < 0 || k >= res->n_pairs) return -1;
+    static const char kOp[4] = {'=', 'X', 'I', 'D'};
+    int64_t pos = 0;
+    char tmp[32];
+    auto put = [&](int op, int64_t len) {
+        const int w = snprintf(tmp, sizeof tmp, "%lld%c", static_cast<long long>(len), kOp[op]);
+        if (buf && pos + w < cap) std::memcpy(buf + pos, tmp, static_cast<size_t>(w));
+        pos += w;
+    };
+    int prev = -1;
+    int64_t run = 0;
+    for (int64_t b = res->cigar_off[k]; b < res->cigar_off[k + 1]; ++b) {
+        const uint8_t v = res->runs[b];
+        const int op = v >> 6;
+        if (op != prev && prev >= 0) {
+            put(prev, run);
+            run = 0;
+        }
+        prev = op;
+        run += (v & 63) + 1;
+    }
+    if (prev >= 0) put(prev, run);
+    if (buf && cap > 0) buf[std::min(pos, cap - 1)] = '\0';
+    return pos;
+}
+
+int sg_pack(const sg_pairs* in, sg_packed_pairs* out) {
+    if (!in || !out) return set_error(SG_INPUT, "null argument");
+    try {
+        auto pk = std::make_unique<Packed>();
+        pack_pairs(in, *pk);
+        *out = pk->view();
+        std::lock_guard<std::mutex> lk(g_owned_mu);
+        packed_registry().push_back(pk.release());
+        return SG_OK;
+    } catch (const Fail& f) {
+        return f.code;
+    }
+}
+
+void sg_packed_free(sg_packed_pairs* p) {
+    if (!p || !p->seq) return;
+    std::lock_guard<std::mutex> lk(g_owned_mu);
+    auto& reg = packed_registry();
+    for (size_t k = 0; k < reg.size(); ++k)
+        if (reg[k]->seq.p == p->seq) {
+            delete reg[k];
+            reg.erase(reg.begin() + static_cast<long>(k));
+            break;
+        }
+    std::memset(p, 0, sizeof *p);
+}
+
+int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int device,
+                      sg_session** out) {
+    *out = nullptr;
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (!pairs || pairs->n_pairs < 0 || pairs->n_pairs > INT32_MAX)
+        return set_error(SG_INPUT, "bad pair batch");
+    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len);
+    if (rc) return rc;
+    if (sg_device_count() <= device || device < 0)
+        return set_error(SG_CUDA, "no CUDA device %d (the GPU path has no CPU fallback)", device);
+    auto s = std::make_unique<sg_session>();
+    try {
+        s->cfg = *cfg;
+        s->rc = run_config(cfg);
+        s->st.init(device);
+        s->n = pairs->n_pairs;
+        bool mixed = false;
+        for (int64_t k = 1; k < s->n && !mixed; ++k)
+            mixed = pairs->text_len[k] + pairs->pat_len[k] != pairs->text_len[0] + pairs->pat_len[0];
+        const Shard sh{pairs, 0, s->n};
+        prep_shard(sh, s->prep, mixed);
+        upload_shard(s->st, sh, s->prep);
+        SG_CUDA_CHECK(cudaStreamSynchronize(s->st.stream));
+    } catch (const Fail& f) {
+        return f.code;
+    }
+    *out = s.release();
+    return SG_OK;
+}
+
+int sg_session_run(sg_session* s, float* device_ms, float* k1_ms) {
+    try {
+        SG_CUDA_CHECK(cudaSetDevice(s->st.device));
+        s->launches = launch_shard(s->st, s->rc, s->prep);
+        SG_CUDA_CHECK(cudaEventSynchronize(s->st.ev[2]));
+        float ms = 0, k1 = 0;
+        SG_CUDA_CHECK(cudaEventElapsedTime(&ms, s->st.ev[0], s->st.ev[2]));
+        SG_CUDA_CHECK(cudaEventElapsedTime(&k1, s->st.ev[0], s->st.ev[1]));
+        if (device_ms) *device_ms = ms;
+        if (k1_ms) *k1_ms = k1;
+        s->ran = true;
+        return SG_OK;
+    } catch (const Fail& f) {
+        return f.code;
+    }
+}
+
+int sg_session_fetch(sg_session* s, sg_results* out) {
+    std::memset(out, 0, sizeof *out);
+    if (!s->ran) return set_error(SG_INPUT, "session has not run");
+    try {
+        SG_CUDA_CHECK(cudaSetDevice(s->st.device));
+        ShardOut so;
+        fetch_small(s->st, s->n, so);
+        if (so.first_bad >= 0)
+            return set_error(SG_INTERNAL, "pair '%lld': %s", static_cast<long long>(so.first_bad),
+                             status_detail(so.first_bad_status));
+        results_alloc(out, s->n, so.run_bytes);
+        if (so.run_bytes)
+            SG_CUDA_CHECK(cudaMemcpyAsync(out->runs, s->st.dense.p, static_cast<size_t>(so.run_bytes),
+                                          cudaMemcpyDeviceToHost, s->st.stream));
+        scatter_small(out, 0, s->n, 0, so);
+        SG_CUDA_CHECK(cudaStreamSynchronize(s->st.stream));
+        finish_totals(out);
+        out->device_ms = so.device_ms;
+        out->kernel_ms = so.k1_ms;
+        out->gpu_launches = s->launches;
+        return SG_OK;
+    } catch (const Fail& f) {
+        sg_results_free(out);
+        return f.code;
+    }
+}
+
+int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* limbs) {
+    if (lanes) *lanes = s->st.lanes;
+    if (sms) *sms = s->st.sms;
+    if (limbs) *limbs = s->rc.L;
+    return SG_OK;
+}
+
+void sg_session_destroy(sg_session* s) { delete s; }
+
+int64_t sg_last_transfer_bytes(int direction) { return direction ? g_last_d2h : g_last_h2d; }
+
+int sg_synth_packed(int cfg_id, int64_t first, int64_t count, sg_packed_pairs* out) {
+    std::memset(out, 0, sizeof *out);
+    sg_synth_spec spec;
+    if (!sg_synth_baseline_spec(cfg_id, &spec)) return set_error(SG_INPUT, "bad config id %d", cfg_id);
+    if (count < 0) count = spec.n_pairs - first;
+    try {
+        // pass 1: lengths (cheap relative to alignment; the generator is replayed)
+        std::vector<int64_t> tl(static_cast<size_t>(count)), pl(static_cast<size_t>(count));
+        int rc = synth_each(spec, first, count,
+                            [&](int64_t k, const uint8_t*, int64_t n, const uint8_t*, int64_t m) {
+                                tl[static_cast<size_t>(k)] = n;
+                                pl[static_cast<size_t>(k)] = m;
+                            });
+        if (rc) return rc;
+        auto pk = std::make_unique<Packed>();
+        layout_offsets(*pk, count, tl.data(), pl.data());
+        uint32_t* seq = pk->seq.as<uint32_t>();
+        const int64_t* to = pk->text_off.as<int64_t>();
+        const int64_t* po = pk->pat_off.as<int64_t>();
+        rc = synth_each(spec, first, count,
+                        [&](int64_t k, const uint8_t* t, int64_t n, const uint8_t* p, int64_t m) {
+                            pack_seq(t, n, seq + to[k] / 16, nullptr, 0);
+                            pack_seq(p, m, seq + po[k] / 16, nullptr, 0);
+                        });
+        if (rc) return rc;
+        pk->any_n = false;
+        *out = pk->view();
+        std::lock_guard<std::mutex> lk(g_owned_mu);
+        packed_registry().push_back(pk.release());
+        return SG_OK;
+    } catch (const Fail& f) {
+        return f.code;
+    }
+}
+
+int sg_synth_codes(int cfg_id, int64_t first, int64_t count, sg_pairs* out) {
+    std::memset(out, 0, sizeof *out);
+    sg_synth_spec spec;
+    if (!sg_synth_baseline_spec(cfg_id, &spec)) return set_error(SG_INPUT, "bad config id %d", cfg_id);
+    if (count < 0) count = spec.n_pairs - first;
+    auto oc = std::make_unique<OwnedCodes>();
+    const size_t c = static_cast<size_t>(count);
+    oc->text_len.resize(c);
+    oc->pat_len.resize(c);
+    int rc = synth_each(spec, first, count,
+                        [&](int64_t k, const uint8_t*, int64_t n, const uint8_t*, int64_t m) {
+                            oc->text_len[static_cast<size_t>(k)] = n;
+                            oc->pat_len[static_cast<size_t>(k)] = m;
+                        });
+    if (rc) return rc;
+    oc->text_off.resize(c);
+    oc->pat_off.resize(c);
+    int64_t ta = 0, pa = 0;
+    for (size_t k = 0; k < c; ++k) {
+        oc->text_off[k] = ta;
+        oc->pat_off[k] = pa;
+        ta += oc->text_len[k];
+        pa += oc->pat_len[k];
+    }
+    oc->text.resize(static_cast<size_t>(std::max<int64_t>(ta, 1)));
+    oc->pattern.resize(static_cast<size_t>(std::max<int64_t>(pa, 1)));
+    rc = synth_each(spec, first, count,
+                    [&](int64_t k, const uint8_t* t, int64_t n, const uint8_t* p, int64_t m) {
+                        std::memcpy(oc->text.data() + oc->text_off[static_cast<size_t>(k)], t,
+                                    static_cast<size_t>(n));
+                        std::memcpy(oc->pattern.data() + oc->pat_off[static_cast<size_t>(k)], p,
+                                    static_cast<size_t>(m));
+                    });
+    if (rc) return rc;
+    out->n_pairs = count;
+    out->text = oc->text.data();
+    out->text_off = oc->text_off.data();
+    out->text_len = oc->text_len.data();
+    out->pattern = oc->pattern.data();
+    out->pat_off = oc->pat_off.data();
+    out->pat_len = oc->pat_len.data();
+    std::lock_guard<std::mutex> lk(g_codes_mu);
+    codes_registry().push_back(oc.release());
+    return SG_OK;
+}
+
+void sg_pairs_free(sg_pairs* p) {
+    if (!p || !p->text) return;
+    std::lock_guard<std::mutex> lk(g_codes_mu);
+    auto& reg = codes_registry();
+    for (size_t k = 0; k < reg.size(); ++k)
+        if (reg[k]->text.data() == p->text) {
+            delete reg[k];
+            reg.erase(reg.begin() + static_cast<long>(k));
+            break;
+        }
+    std::memset(p, 0, sizeof *p);
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// K1 `window_align`: the fused GenASM-DC + GenASM-TB + window loop (sm_100a).
+//
+// Replaces compute_dc (proj/src/dp.cpp:104-231), traceback
+// (proj/src/traceback.cpp:56-113) and the window loop of align
+// (proj/src/aligner.cpp:28-85). See DESIGN.md §3 for the derivation; summary:
+//
+//  * One thread owns one pair (SIMT across pairs). A persistent grid pulls
+//    pairs from an atomic queue (optionally in a caller-given order).
+//  * Bit vectors are 32L-bit registers ("limbs"), logical position q = pL + r
+//    lives in limb r, machine bit 31-p. The pattern is right-aligned
+//    (bit j at q = j + 32L - m_w), so the end-of-pattern boundary bit
+//    (proj/include/scrooge/dp.hpp:145-154) always enters at the LSB of limb
+//    L-1 and a DP shift costs ONE integer multiply-add (x*2 + b, FMA pipe):
+//    the other limbs are renamed, not moved.
+//  * DC sweeps columns i = n-1..0 and keeps R rows of the column in registers
+//    (rows d0..d0+R-1, a "chunk"). Early termination is per lane at chunk
+//    granularity: a lane whose window is not solved continues with the next
+//    chunk (the last row of each column is parked in a global scratch row)
+//    while its warp-mates already trace back or start their next window.
+//  * SENE/DENT: nothing of R is retained. For the DENT region (columns
+//    < C, C >= W-O) each cell keeps a 2-bit traceback code accumulated
+//    during DC from the SENE regeneration rule evaluated at the cell's own
+//    row (traceback.cpp:35-54): Match <=> t_i == p_j; Sub <=> D(i+1,j+1) <
+//    D(i,j); Del <=> D(i+1,j) < D(i,j); else Ins.
+//  * TB walks those codes from (0,0) in lock step across the lanes that
+//    solved their window. A final window wider than C continues as a new
+//    DC segment on the untouched suffix (suffix distances are intrinsic).
+#pragma once
+
+#include <cstdint>
+
+namespace sgk {
+
+// Per-pair status (low 16 bits = kind as the C ABI's SG_* codes, high = detail).
+enum : int32_t {
+    kStOk = 0,
+    kStInternal = 3,
+    kDetBudgetI = 1 << 16,      // traceback.cpp:76-78
+    kDetBudgetD = 2 << 16,      // traceback.cpp:84-86
+    kDetLeftover = 3 << 16,     // traceback.cpp:110-111
+    kDetWatchdog = 4 << 16,     // aligner.cpp:81-82
+    kDetNoStep = 5 << 16,       // traceback.cpp:105-106
+    kDetSegment = 6 << 16,      // continuation segment disagrees with the budget
+};
+
+struct AlignParams {
+    const uint32_t* seq;      // 2-bit packed bases, 16 per word, base k at bits 2(k%16)
+    const uint32_t* nmask;    // 1 bit per base (same base offsets), may be null
+    const int64_t* text_off;  // base offset of each text
+    const int64_t* pat_off;   // base offset of each pattern
+    const int32_t* text_len;
+    const int32_t* pat_len;
+    const uint8_t* has_n;     // per pair: any non-ACGT base (may be null)
+    const int32_t* order;     // processing order (null = identity)
+    int32_t n_pairs;
+    int32_t W, O, et, policy; // policy: 0 BaselineEdges, 1 SeneEntries, 2 DentTrimmed (counters)
+    // outputs
+    int32_t* distance;
+    int32_t* windows;
+    int32_t* status;
+    int32_t* out_bytes;       // run bytes per pair
+    uint64_t* counters;       // [n_pairs][7] (InstrumentationCounters order) or null
+    const int64_t* bound_off; // byte offset (4-aligned) of each pair's run region in scratch
+    uint32_t* scratch;        // run bytes, (op << 6) | (len - 1)
+    uint32_t* bnd;            // parked rows: per warp [32L + 1 columns][32 lanes][L]
+    unsigned int* next_pair;  // work queue head
+};
+
+// Launch K1 for limb count L (W <= 32L). Returns cudaError_t as int.
+int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_block,
+                        void* stream);
+// Bytes of parked-row scratch needed for `total_warps` warps at limb count L.
+size_t bnd_scratch_bytes(int L, long long total_warps);
+// Shared memory per block and the warps per block used for L.
+int k1_warps_per_block(int L);
+size_t k1_smem_bytes(int L);
+int k1_max_blocks_per_sm(int L);
+
+// K2/K3: exclusive scan of the per-pair run byte counts (dense_off has n+1
+// entries, the total last) and compaction of the bounded run regions into one
+// dense byte buffer.
+int launch_cigar_offsets(const int32_t* out_bytes, int64_t* dense_off, int32_t n, void* temp,
+                         size_t temp_bytes, void* stream);
+size_t cigar_offsets_temp_bytes(int32_t n);
+int launch_cigar_compact(const uint32_t* scratch, const int64_t* bound_off,
+                         const int64_t* dense_off, const int32_t* out_bytes, uint8_t* dense,
+                         int32_t n, void* stream);
+
+}  // namespace sgk

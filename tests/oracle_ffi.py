@@ -1,0 +1,153 @@
+"""ctypes bindings for the C oracle (oracle/_build/liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: the oracle is the CPU checker the GPU path is
+compared against. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+LIB_PATH = os.path.join(ORACLE_DIR, "_build", "liboracle.so")
+REF_TOOL = os.path.join(ORACLE_DIR, "_ref", "ref_tool")
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [("W", C.c_int32), ("O", C.c_int32), ("sene", C.c_uint8), ("dent", C.c_uint8),
+                ("et", C.c_uint8), ("single_window", C.c_uint8), ("k_single", C.c_int32)]
+
+
+class OrcCounters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "stored_bits", "table_writes", "table_reads", "rows_computed", "cells_computed",
+        "rows_possible", "baseline_equiv_bits")]
+
+
+class OrcResult(C.Structure):
+    _fields_ = [("found", C.c_int32), ("distance", C.c_int64), ("windows", C.c_int32),
+                ("n_runs", C.c_int64), ("ops", C.POINTER(C.c_char)),
+                ("lens", C.POINTER(C.c_int64)), ("counters", OrcCounters)]
+
+
+class SynthSpec(C.Structure):
+    _fields_ = [("n_pairs", C.c_int64), ("seed", C.c_uint64), ("read_min", C.c_int32),
+                ("read_max", C.c_int32), ("slack_abs", C.c_int32), ("slack_frac", C.c_double),
+                ("rate_min", C.c_double), ("rate_max", C.c_double), ("mix_sub", C.c_double),
+                ("mix_ins", C.c_double), ("mix_del", C.c_double),
+                ("frac_uncorrelated", C.c_double)]
+
+
+_lib = None
+
+
+def ensure_built() -> None:
+    if not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", ORACLE_DIR, "all"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        ensure_built()
+        L = C.CDLL(LIB_PATH)
+        L.orc_align.argtypes = [C.POINTER(OrcConfig), C.c_char_p, C.c_int64, C.c_char_p,
+                                C.c_int64, C.POINTER(OrcResult), C.c_char_p, C.c_size_t]
+        L.orc_align.restype = C.c_int
+        L.orc_result_free.argtypes = [C.POINTER(OrcResult)]
+        L.orc_last_window_count.restype = C.c_int64
+        L.orc_last_window_stats.argtypes = [C.POINTER(C.c_int32)] * 3 + [C.c_int64]
+        L.sg_synth_baseline_spec.argtypes = [C.c_int, C.POINTER(SynthSpec)]
+        L.sg_synth_max_text.argtypes = [C.POINTER(SynthSpec)]
+        L.sg_synth_max_text.restype = C.c_int64
+        L.sg_synth_max_pattern.argtypes = [C.POINTER(SynthSpec)]
+        L.sg_synth_max_pattern.restype = C.c_int64
+        L.sg_synth_pair.argtypes = [C.POINTER(SynthSpec), C.c_int64, C.c_char_p,
+                                    C.POINTER(C.c_int64), C.c_char_p, C.POINTER(C.c_int64)]
+        _lib = L
+    return _lib
+
+
+COUNTER_NAMES = [n for n, _ in OrcCounters._fields_]
+
+
+@dataclass
+class Alignment:
+    found: bool
+    distance: int
+    cigar: str
+    windows: int
+    counters: dict = field(default_factory=dict)
+
+
+class OracleError(Exception):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def align(text: bytes, pattern: bytes, W=64, O=33, sene=True, dent=True, et=True,
+          single_window=False, k_single=1024) -> Alignment:
+    """Oracle align() on 1-byte base codes (0..3 ACGT, 4 other)."""
+    L = lib()
+    cfg = OrcConfig(W, O, int(sene), int(dent), int(et), int(single_window), k_single)
+    res = OrcResult()
+    err = C.create_string_buffer(512)
+    rc = L.orc_align(C.byref(cfg), bytes(text), len(text), bytes(pattern), len(pattern),
+                     C.byref(res), err, len(err))
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    cig = "".join(f"{res.lens[k]}{res.ops[k].decode()}" for k in range(res.n_runs))
+    out = Alignment(bool(res.found), res.distance, cig if res.found else "*", res.windows,
+                    {n: getattr(res.counters, n) for n in COUNTER_NAMES})
+    L.orc_result_free(C.byref(res))
+    return out
+
+
+def window_stats():
+    """(d_opt, n_w, m_w) of every window of the last align() on this thread."""
+    L = lib()
+    n = L.orc_last_window_count()
+    a = (C.c_int32 * n)()
+    b = (C.c_int32 * n)()
+    c = (C.c_int32 * n)()
+    L.orc_last_window_stats(a, b, c, n)
+    return list(a), list(b), list(c)
+
+
+def baseline_spec(cfg_id: int) -> SynthSpec:
+    s = SynthSpec()
+    if not lib().sg_synth_baseline_spec(cfg_id, C.byref(s)):
+        raise ValueError(cfg_id)
+    return s
+
+
+def synth_pair(spec: SynthSpec, p: int):
+    L = lib()
+    tb = C.create_string_buffer(L.sg_synth_max_text(C.byref(spec)))
+    pb = C.create_string_buffer(L.sg_synth_max_pattern(C.byref(spec)))
+    n = C.c_int64()
+    m = C.c_int64()
+    L.sg_synth_pair(C.byref(spec), p, tb, C.byref(n), pb, C.byref(m))
+    return tb.raw[:n.value], pb.raw[:m.value]
+
+
+def encode(s: str) -> bytes:
+    """encode_sequence, proj/include/scrooge/sequence.hpp:19-37."""
+    tbl = {"A": 0, "C": 1, "G": 2, "T": 3, "a": 0, "c": 1, "g": 2, "t": 3}
+    return bytes(tbl.get(ch, 4) for ch in s)
+
+
+def decode(b: bytes) -> str:
+    return "".join("ACGTN"[min(x, 4)] for x in b)
+
+
+def fnv1a(s: str) -> str:
+    h = 1469598103934665603
+    for ch in s.encode():
+        h = ((h ^ ch) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
