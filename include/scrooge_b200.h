@@ -174,6 +174,11 @@ int sg_session_fetch(sg_session* s, sg_results* out);
 int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* limbs);
 void sg_session_destroy(sg_session* s);
 
+/* Measured integer-ALU issue rate of `device` (LOP3 lane-ops per clock per SM,
+ * the clock the microbenchmark ran at, and lane-ops/s) — the roofline
+ * denominator for K1. */
+int sg_alu_peak(int device, double* ops_per_clk_per_sm, double* sm_mhz, double* ops_per_s);
+
 /* Seeded synthetic pairs of the BASELINE configs (paper_2208_09985_b200/csrc/
  * synth.h), generated straight into packed form with host threads. */
 int sg_synth_packed(int cfg_id, int64_t first, int64_t count, sg_packed_pairs* out);

@@ -8,6 +8,7 @@
  */
 #include "genasm_oracle.h"
 
+#include <pthread.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -460,4 +461,85 @@ int64_t orc_cigar_string(const orc_result* r, char* buf, int64_t cap) {
     }
     if (buf && pos < cap) buf[pos] = '\0';
     return pos;
+}
+
+/* ---- replay checks (test-side; proj/src/cigar.cpp:70-107) ---- */
+static int bases_match(uint8_t a, uint8_t b) { return a == b && a < 4; }
+
+int64_t orc_replay_runs(const uint8_t* text, int64_t n, const uint8_t* pattern, int64_t m,
+                        const uint8_t* runs, int64_t nbytes) {
+    int64_t i = 0, j = 0, edits = 0;
+    for (int64_t b = 0; b < nbytes; ++b) {
+        const int op = runs[b] >> 6;
+        const int64_t len = (runs[b] & 63) + 1;
+        for (int64_t r = 0; r < len; ++r) {
+            switch (op) {
+                case 0:
+                    if (i >= n || j >= m || !bases_match(text[i], pattern[j])) return -1;
+                    ++i, ++j;
+                    break;
+                case 1:
+                    if (i >= n || j >= m || bases_match(text[i], pattern[j])) return -1;
+                    ++i, ++j, ++edits;
+                    break;
+                case 2:
+                    if (j >= m) return -1;
+                    ++j, ++edits;
+                    break;
+                default:
+                    if (i >= n) return -1;
+                    ++i, ++edits;
+                    break;
+            }
+        }
+    }
+    return i == n && j == m ? edits : -1;
+}
+
+typedef struct {
+    int64_t lo, hi, bad;
+    const uint8_t *text, *pattern, *runs;
+    const int64_t *text_off, *text_len, *pat_off, *pat_len, *cigar_off, *distance;
+} replay_job;
+
+static void* replay_worker(void* arg) {
+    replay_job* j = (replay_job*)arg;
+    for (int64_t k = j->lo; k < j->hi; ++k) {
+        const int64_t e = orc_replay_runs(j->text + j->text_off[k], j->text_len[k],
+                                          j->pattern + j->pat_off[k], j->pat_len[k],
+                                          j->runs + j->cigar_off[k],
+                                          j->cigar_off[k + 1] - j->cigar_off[k]);
+        if (e < 0 || e != j->distance[k]) ++j->bad;
+    }
+    return NULL;
+}
+
+int64_t orc_replay_batch(int64_t n_pairs, const uint8_t* text, const int64_t* text_off,
+                         const int64_t* text_len, const uint8_t* pattern, const int64_t* pat_off,
+                         const int64_t* pat_len, const uint8_t* runs, const int64_t* cigar_off,
+                         const int64_t* distance, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 128) threads = 128;
+    pthread_t th[128];
+    replay_job jobs[128];
+    const int64_t chunk = (n_pairs + threads - 1) / threads;
+    int started = 0;
+    for (int t = 0; t < threads; ++t) {
+        replay_job* j = &jobs[t];
+        j->lo = t * chunk;
+        j->hi = j->lo + chunk < n_pairs ? j->lo + chunk : n_pairs;
+        j->bad = 0;
+        j->text = text; j->pattern = pattern; j->runs = runs;
+        j->text_off = text_off; j->text_len = text_len; j->pat_off = pat_off;
+        j->pat_len = pat_len; j->cigar_off = cigar_off; j->distance = distance;
+        if (j->lo >= j->hi) break;
+        pthread_create(&th[t], NULL, replay_worker, j);
+        ++started;
+    }
+    int64_t bad = 0;
+    for (int t = 0; t < started; ++t) {
+        pthread_join(th[t], NULL);
+        bad += jobs[t].bad;
+    }
+    return bad;
 }

@@ -57,6 +57,19 @@ void orc_result_free(orc_result* r);
  * or the required size when buf is too small. */
 int64_t orc_cigar_string(const orc_result* r, char* buf, int64_t cap);
 
+/* validate_replay (proj/src/cigar.cpp:70-107) over the compact run bytes of
+ * the GPU path ((op << 6) | (len - 1), op 0 '=', 1 'X', 2 'I', 3 'D';
+ * same-op bytes continue a run). Returns the edit count (X + I + D), or -1 if
+ * the CIGAR does not transform text into pattern. */
+int64_t orc_replay_runs(const uint8_t* text, int64_t n, const uint8_t* pattern, int64_t m,
+                        const uint8_t* runs, int64_t nbytes);
+/* Same check for many pairs at once (threads); returns the number of pairs
+ * that fail or whose edit count differs from distance[k]. */
+int64_t orc_replay_batch(int64_t n_pairs, const uint8_t* text, const int64_t* text_off,
+                         const int64_t* text_len, const uint8_t* pattern, const int64_t* pat_off,
+                         const int64_t* pat_len, const uint8_t* runs, const int64_t* cigar_off,
+                         const int64_t* distance, int threads);
+
 /* Per-window statistics hook: d_opt and window geometry of every window of
  * the last orc_align call on this thread (for ALG_OPS/design studies). */
 int64_t orc_last_window_count(void);

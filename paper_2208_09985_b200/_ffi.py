@@ -23,7 +23,7 @@ EXPORTS = (
     "sg_cigar_string", "sg_cigar_runs", "sg_pack", "sg_packed_free",
     "sg_last_transfer_bytes", "sg_session_create", "sg_session_run", "sg_session_fetch",
     "sg_session_info", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
-    "sg_pairs_free",
+    "sg_pairs_free", "sg_alu_peak",
 )
 
 
@@ -99,6 +99,7 @@ def load(build_if_missing: bool = True):
     L.sg_synth_codes.argtypes = [C.c_int, C.c_int64, C.c_int64, P(SgPairs)]
     L.sg_pairs_free.argtypes = [P(SgPairs)]
     L.sg_pairs_free.restype = None
+    L.sg_alu_peak.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_double)]
     _lib = L
     return L
 

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libscrooge_b200.so")
-SOURCES = ["window_align.cu", "host.cu", "synth.c"]
+SOURCES = ["window_align.cu", "host.cu", "peak.cu", "synth.c"]
 HEADERS = ["window_align.cuh", "synth.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

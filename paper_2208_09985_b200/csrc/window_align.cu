@@ -17,9 +17,12 @@ template <> struct KCfg<1> { static constexpr int R = 8, C = 32, WARPS = 4; };
 template <> struct KCfg<2> { static constexpr int R = 8, C = 40, WARPS = 4; };
 template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
 
+template <int L> __host__ __device__ constexpr int txt_words() { return (32 * L / 8) * 32 * 2; }
 template <int L> __host__ __device__ constexpr int pq_words() { return KCfg<L>::C * 2 * L * 32; }
 template <int L> __host__ __device__ constexpr int pm_words() { return 5 * L * 32; }
-template <int L> __host__ __device__ constexpr int warp_smem_words() { return pq_words<L>() + pm_words<L>(); }
+template <int L> __host__ __device__ constexpr int warp_smem_words() {
+    return txt_words<L>() + pq_words<L>() + pm_words<L>();
+}
 
 // ---------------------------------------------------------------- bit utils
 
@@ -46,6 +49,16 @@ template <int S> __device__ __forceinline__ constexpr uint32_t stride_mask() {
 }
 
 __device__ __forceinline__ uint32_t shr_sat(uint32_t x, int s) { return s >= 32 ? 0u : x >> s; }
+
+// 4 two-bit fields (bits 0..7) -> 4 bytes; 4 bits -> 4 bytes of 0/1.
+__device__ __forceinline__ uint32_t spread4(uint32_t a) {
+    a &= 0xFFu;
+    return (a | (a << 6) | (a << 12) | (a << 18)) & 0x03030303u;
+}
+__device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
+    b &= 0xFu;
+    return (b | (b << 7) | (b << 14) | (b << 21)) & 0x01010101u;
+}
 
 // x*2 + b on the FMA pipe (IMAD): the DP shift of limb 0 into limb L-1.
 __device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t b) {
@@ -126,68 +139,280 @@ template <int L> __device__ __forceinline__ uint32_t init_limb(int d, int l) {
     return z >= 32 ? 0u : (~0u << z);
 }
 
-// One column i of a chunk: rows d0..d0+R-1. col[r] holds R[i+1][d0+r] on
-// entry and R[i][d0+r] on exit; ic[r] holds the shifted limb of I(i+1, d),
-// which is S(i, d) (dp.cpp:193-194 boundary terms coincide).
-//   I = shl1(R[i][d-1], [n-i > d-1]);  D = R[i+1][d-1];
-//   S = shl1(R[i+1][d-1], [n-i-1 > d-1]);  M = shl1(R[i+1][d], [n-i-1 > d]) | PM[t_i]
-//   R[i][d] = I & D & S & M                         (proj/src/dp.cpp:187-211)
-// With e = (n - i) - d0 the boundary bits are [e >= r] and [e >= r + 2].
-// CAPTURE accumulates the traceback events of the column:
-//   X |= R & ~shl1(R[i+1][d])   (a D(i+1,j+1) < D(i,j) event)
-//   Y |= R & ~R[i+1][d]         (a D(i+1,j)   < D(i,j) event)
-template <int L, int R, bool FAST, bool CAPTURE>
-__device__ __forceinline__ void dc_column(uint32_t (&col)[R][L], uint32_t (&ic)[R],
-                                          uint32_t (&diag0)[L], const uint32_t (&north0)[L],
-                                          const uint32_t (&pm)[L], int e, uint32_t (&X)[L],
-                                          uint32_t (&Y)[L]) {
-    uint32_t diag[L], north[L];
-#pragma unroll
-    for (int l = 0; l < L; ++l) {
-        diag[l] = diag0[l];
-        north[l] = north0[l];
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const uint32_t bI = FAST ? 1u : static_cast<uint32_t>(e >= r);
-        const uint32_t bM = FAST ? 1u : static_cast<uint32_t>(e >= r + 2);
-        uint32_t east[L], I[L], M[L], S[L], Rv[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) east[l] = col[r][l];
-#pragma unroll
-        for (int l = 0; l + 1 < L; ++l) {
-            I[l] = north[l + 1];
-            M[l] = east[l + 1];
-            S[l] = diag[l + 1];
-        }
-        I[L - 1] = dp_shift(north[0], bI);
-        M[L - 1] = dp_shift(east[0], bM);
-        S[L - 1] = ic[r];
-#pragma unroll
-        for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & S[l] & (M[l] | pm[l]);
-        if (CAPTURE) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                X[l] |= Rv[l] & ~M[l];
-                Y[l] |= Rv[l] & ~east[l];
-            }
-        }
-        ic[r] = I[L - 1];
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            diag[l] = east[l];
-            north[l] = Rv[l];
-            col[r][l] = Rv[l];
-        }
-    }
-#pragma unroll
-    for (int l = 0; l < L; ++l) diag0[l] = north0[l];
-}
-
 __device__ __forceinline__ int warp_max(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
     return v;
+}
+
+// ---------------------------------------------------------------- skewed DC sweep
+//
+// One chunk (rows d0..d0+R-1) of GenASM-DC over all columns of a window as a
+// skewed wavefront: at step s row r works on column col0(s) + r, where
+// col0(s) = S0 - s is row 0's column. The R cells of a step are independent
+// (each needs only the previous step's values), which gives the warp R-way
+// instruction-level parallelism instead of an R-long dependency chain.
+// Columns >= n_w are "virtual": pattern mask all ones and boundary bits 0,
+// which reproduce the init column R[n][d] exactly, so the fill of the
+// wavefront needs no special code. The pattern masks and the traceback event
+// accumulators of the R columns in flight live in rings indexed by the step
+// at which row 0 entered the column; unrolling the step loop by R makes every
+// ring index static (no register moves).
+template <int L, int R>
+struct Sweep {
+    uint32_t v[R][L];       // latest value of row r (R[col_r][d0 + r])
+    uint32_t dg[R][L];      // diag input of row r at its next step
+    uint32_t ic[R];         // S(col_r - 1, d) = shifted limb of I(col_r, d)
+    uint32_t pmq[R][L];     // pattern mask ring
+    uint32_t acc[R][2][L];  // X / Y event ring
+};
+
+// Step U (static) of a group. MODE 0: fast, no capture; 1: fast with capture;
+// 2: slow (explicit boundary bits) with capture. `g` = n_w - S0 - d0 + s; the
+// boundary bits of row r are [g >= 2r] (plus d == 0 for row 0) and [g >= 2r+2]
+// (dp.cpp:187-195 with c = n_w - col: [c > d-1], [c-1 > d]).
+template <int L, int R, int U, int MODE>
+__device__ __forceinline__ void sweep_step(Sweep<L, R>& S, const uint32_t (&north0)[L],
+                                           const uint32_t (&pm0)[L], int g, bool z0) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) S.pmq[U][l] = pm0[l];
+    uint32_t t[R + 1];
+    if (MODE == 2) {
+#pragma unroll
+        for (int k = 0; k <= R; ++k) t[k] = static_cast<uint32_t>(g >= 2 * k);
+        t[0] |= static_cast<uint32_t>(z0);
+    }
+#pragma unroll
+    for (int r = R - 1; r >= 0; --r) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int slot = (U - r) & (R - 1);
+        uint32_t north[L], east[L], diag[L], pm[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            north[l] = r == 0 ? north0[l] : S.v[r == 0 ? 0 : r - 1][l];
+            east[l] = S.v[r][l];
+            diag[l] = S.dg[r][l];
+            pm[l] = S.pmq[slot][l];
+        }
+        const uint32_t bI = MODE == 2 ? t[r] : 1u;
+        const uint32_t bM = MODE == 2 ? t[r + 1] : 1u;
+        uint32_t I[L], M[L], Sv[L], Rv[L];
+#pragma unroll
+        for (int l = 0; l + 1 < L; ++l) {
+            I[l] = north[l + 1];
+            M[l] = east[l + 1];
+            Sv[l] = diag[l + 1];
+        }
+        I[L - 1] = dp_shift(north[0], bI);
+        M[L - 1] = dp_shift(east[0], bM);
+        Sv[L - 1] = S.ic[r];
+#pragma unroll
+        for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | pm[l]);
+        if (MODE != 0) {
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const uint32_t x = Rv[l] & ~M[l], y = Rv[l] & ~east[l];
+                if (r == 0) {
+                    S.acc[slot][0][l] = x;
+                    S.acc[slot][1][l] = y;
+                } else {
+                    S.acc[slot][0][l] |= x;
+                    S.acc[slot][1][l] |= y;
+                }
+            }
+        }
+        S.ic[r] = I[L - 1];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            if (r + 1 < R) S.dg[r + 1 < R ? r + 1 : 0][l] = east[l];
+            S.v[r][l] = Rv[l];
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) S.dg[0][l] = north0[l];
+}
+
+// Drain step K (1..R-1, static): row 0's column is -K; rows r >= K finish
+// columns r-K. Boundary bits explicit (MODE 2 rule).
+template <int L, int R, int K>
+__device__ __forceinline__ void drain_step(Sweep<L, R>& S, int g) {
+    uint32_t t[R + 1];
+#pragma unroll
+    for (int k = 0; k <= R; ++k) t[k] = static_cast<uint32_t>(g >= 2 * k);
+#pragma unroll
+    for (int r = R - 1; r >= K; --r) {
+        const int slot = (R - 1 + K - r) & (R - 1);
+        uint32_t north[L], east[L], diag[L], pm[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            north[l] = S.v[r - 1][l];
+            east[l] = S.v[r][l];
+            diag[l] = S.dg[r][l];
+            pm[l] = S.pmq[slot][l];
+        }
+        uint32_t I[L], M[L], Sv[L], Rv[L];
+#pragma unroll
+        for (int l = 0; l + 1 < L; ++l) {
+            I[l] = north[l + 1];
+            M[l] = east[l + 1];
+            Sv[l] = diag[l + 1];
+        }
+        I[L - 1] = dp_shift(north[0], t[r]);
+        M[L - 1] = dp_shift(east[0], t[r + 1]);
+        Sv[L - 1] = S.ic[r];
+#pragma unroll
+        for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | pm[l]);
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            S.acc[slot][0][l] |= Rv[l] & ~M[l];
+            S.acc[slot][1][l] |= Rv[l] & ~east[l];
+        }
+        S.ic[r] = I[L - 1];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            if (r + 1 < R) S.dg[r + 1 < R ? r + 1 : 0][l] = east[l];
+            S.v[r][l] = Rv[l];
+        }
+    }
+}
+
+// Side effects of the column row R-1 just finished (static ring SLOT): park
+// its value for the next chunk and fold the column's events into the 2-bit
+// traceback codes P = X | ~PM, Q = PM & (X | Y)  (M=(1,0) S=(1,1) D=(0,1) I=(0,0)).
+template <int L, int R, int C, int SLOT, bool CAP>
+__device__ __forceinline__ void finish_col(const Sweep<L, R>& S, int colf, int n_w, int d0,
+                                           uint32_t* __restrict__ pq, uint32_t* __restrict__ bnd,
+                                           int lane) {
+    if (colf >= 0 && colf < n_w) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) bnd[(colf * 32 + lane) * L + l] = S.v[R - 1][l];
+        if (CAP && colf < C) {
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                uint32_t* pp = pq + ((colf * 2 + 0) * L + l) * 32 + lane;
+                uint32_t* qp = pq + ((colf * 2 + 1) * L + l) * 32 + lane;
+                const uint32_t pm = S.pmq[SLOT][l];
+                const uint32_t x = S.acc[SLOT][0][l], y = S.acc[SLOT][1][l];
+                const uint32_t pold = d0 > 0 ? *pp : ~pm;
+                const uint32_t qold = d0 > 0 ? *qp : 0u;
+                *pp = pold | x;
+                *qp = qold | (pm & (x | y));
+            }
+        }
+    }
+}
+
+// Bit j = 0 of row r's value at column 0 (the d_opt test, dp.cpp:222).
+template <int L, int R>
+__device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0, int p0) {
+    uint32_t v = S.v[r][0];
+#pragma unroll
+    for (int l = 1; l < L; ++l) v = r0 == l ? S.v[r][l] : v;
+    return (v >> (31 - p0)) & 1u;
+}
+
+template <int L, int R, int C, int MODE>
+__device__ __forceinline__ void sweep_group(Sweep<L, R>& S, const uint32_t (&nb)[R][L],
+                                            uint64_t codes8, int col_top,
+                                            const uint32_t* __restrict__ pmv, int g0, bool z0,
+                                            int n_w, int d0, uint32_t* __restrict__ pq,
+                                            uint32_t* __restrict__ bnd, int lane) {
+#define SG_STEP(U)                                                                          \
+    if ((U) < R) {                                                                          \
+        const int col0 = col_top - (U);                                                     \
+        const int code = static_cast<int>((codes8 >> (8 * (col0 & 7))) & 0xFFu);            \
+        uint32_t pm0[L];                                                                    \
+        _Pragma("unroll") for (int l = 0; l < L; ++l) pm0[l] = pmv[(code * 32 + lane) * L + l]; \
+        sweep_step<L, R, ((U) < R ? (U) : 0), MODE>(S, nb[(U) < R ? (U) : 0], pm0, g0 + (U), z0); \
+        finish_col<L, R, C, (((U) + 1) & (R - 1)), MODE != 0>(S, col0 + R - 1, n_w, d0, pq, bnd, \
+                                                            lane);                           \
+    }
+    SG_STEP(0) SG_STEP(1) SG_STEP(2) SG_STEP(3) SG_STEP(4) SG_STEP(5) SG_STEP(6) SG_STEP(7)
+#undef SG_STEP
+}
+
+template <int L, int R, int C, int K>
+__device__ __forceinline__ void drain_one(Sweep<L, R>& S, int g, int n_w, int d0, uint32_t* pq,
+                                          uint32_t* bnd, int lane, int r0, int p0, int& fr) {
+    if (K < R) {
+        drain_step<L, R, (K < R ? K : 1)>(S, g);
+        finish_col<L, R, C, (K & (R - 1)), true>(S, R - 1 - K, n_w, d0, pq, bnd, lane);
+        if (fr < 0 && !top_bit<L, R>(S, K < R ? K : 0, r0, p0)) fr = K;
+    }
+}
+
+// One chunk of rows d0..d0+R-1 over columns n_w-1..0 (n_w = 0: inactive lane).
+// Returns the first row r of the chunk with bit j=0 of R[0][d0+r] clear, or -1.
+template <int L, int R, int C>
+__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max,
+                                        const uint32_t* __restrict__ pmv,
+                                        const uint64_t* __restrict__ txt, uint32_t* __restrict__ pq,
+                                        uint32_t* __restrict__ bnd, int lane) {
+    constexpr int WB = 32 * L;
+    static_assert((R & (R - 1)) == 0 && R <= 8 && WB % R == 0, "R must be a power of two <= 8");
+    Sweep<L, R> S;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int d = d0 + r;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            S.v[r][l] = init_limb<L>(d, l);
+            S.dg[r][l] = init_limb<L>(d - 1, l);
+            S.pmq[r][l] = ~0u;
+            S.acc[r][0][l] = S.acc[r][1][l] = 0u;
+        }
+        // I(n, d) = shl1(R[n][d-1], [d == 0]) with R[n][-1] = ones
+        S.ic[r] = d == 0 ? ~0u : (init_limb<L>(d - 1, 0) << 1);
+    }
+    const int tsteps = ((n_max + R - 1) / R) * R;
+    const int S0 = tsteps - 1;
+    const bool z0 = d0 == 0;
+    uint32_t init_north[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) init_north[l] = init_limb<L>(d0 - 1, l);
+    // row-0 north inputs (the parked row d0-1), prefetched one group ahead
+    uint32_t nb[R][L], nbn[R][L];
+    auto fetch_nb = [&](uint32_t (&dst)[R][L], int col_top) {
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int col = col_top - u;
+            const bool real = col >= 0 && col < n_w && d0 > 0;
+#pragma unroll
+            for (int l = 0; l < L; ++l)
+                dst[u][l] = real ? bnd[(col * 32 + lane) * L + l] : init_north[l];
+        }
+    };
+    fetch_nb(nb, S0);
+    for (int sg = 0; sg < tsteps; sg += R) {
+        const int col_top = S0 - sg;
+        if (sg + R < tsteps) fetch_nb(nbn, col_top - R);
+        const uint64_t codes8 = txt[(col_top >> 3) * 32 + lane];
+        const int g0 = n_w - S0 - d0 + sg;
+        const bool slow = __any_sync(kFull, n_w > 0 && g0 < 2 * R);
+        if (slow)
+            sweep_group<L, R, C, 2>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
+        else if (col_top - R + 1 < C)
+            sweep_group<L, R, C, 1>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
+        else
+            sweep_group<L, R, C, 0>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+#pragma unroll
+            for (int l = 0; l < L; ++l) nb[u][l] = nbn[u][l];
+    }
+    const int off = WB - m_w;
+    const int r0 = off % L, p0 = off / L;
+    int fr = top_bit<L, R>(S, 0, r0, p0) ? -1 : 0;
+    const int gd = n_w - S0 - d0 + tsteps;  // g at drain step 1 minus 1
+    drain_one<L, R, C, 1>(S, gd + 0, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 2>(S, gd + 1, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 3>(S, gd + 2, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 4>(S, gd + 3, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 5>(S, gd + 4, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 6>(S, gd + 5, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    drain_one<L, R, C, 7>(S, gd + 6, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    return fr;
 }
 
 // ------------------------------------------------------------------ K1
@@ -199,8 +424,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    uint32_t* const pq = smem + wib * warp_smem_words<L>();  // [C][2][L][32]
-    uint32_t* const pmv = pq + pq_words<L>();                 // [5][32][L]
+    uint64_t* const txt = reinterpret_cast<uint64_t*>(smem + wib * warp_smem_words<L>());
+    uint32_t* const pq = smem + wib * warp_smem_words<L>() + txt_words<L>();  // [C][2][L][32]
+    uint32_t* const pmv = pq + pq_words<L>();                                 // [5][32][L]
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
     uint32_t* const bnd = P.bnd + gwarp * (WB + 1) * 32 * L;  // [WB+1][32][L]
 
@@ -220,7 +446,6 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     int d0 = 0, found_d = -1, expect_d = -1;
     int dist = 0, nwin = 0, status = 0;
     long long window_cap = 0;
-    uint32_t tw[2 * L], tn[L];
     // output
     uint32_t* outw = nullptr;
     int out_bytes = 0, cur_op = -1, acc_n = 0;
@@ -282,10 +507,25 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
             pmv[(2 * 32 + lane) * L + r] = lo | ~hi | nn;
             pmv[(3 * 32 + lane) * L + r] = ~lo | ~hi | nn;
         }
+        uint32_t tw[2 * L], tn[L];
         load_codes<2 * L>(P.seq, tbase + toff, tw);
 #pragma unroll
         for (int l = 0; l < L; ++l) tn[l] = 0;
         if (hasn) load_bits<L>(P.nmask, tbase + toff, tn);
+        // text codes as bytes, 8 columns per u64; non-ACGT and columns >= n_w -> 4
+#pragma unroll
+        for (int b = 0; b < WB / 8; ++b) {
+            const uint32_t x = (tw[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
+            uint64_t c = static_cast<uint64_t>(spread4(x)) |
+                         (static_cast<uint64_t>(spread4(x >> 8)) << 32);
+            const uint32_t nb8 = (tn[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+            uint64_t m = (static_cast<uint64_t>(spread4bits(nb8)) |
+                          (static_cast<uint64_t>(spread4bits(nb8 >> 4)) << 32)) * 0xFFull;
+            const int valid = n_w - 8 * b;
+            if (valid < 8) m |= valid <= 0 ? ~0ull : (~0ull << (8 * valid));
+            c = (c & ~m) | (0x0404040404040404ull & m);
+            txt[b * 32 + lane] = c;
+        }
     };
 
     // Sets up the next logical window of the current pair (aligner.cpp:44-64).
@@ -376,106 +616,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         if (!__any_sync(kFull, in_dc)) break;
 
         // ------------------------------------------------ DC: one chunk
-        uint32_t col[R][L], ic[R], diag0[L], X[L], Y[L];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int d = d0 + r;
-#pragma unroll
-            for (int l = 0; l < L; ++l) col[r][l] = init_limb<L>(d, l);
-            // I(n, d) = shl1(R[n][d-1], [d == 0]); R[n][-1] = ones
-            ic[r] = d == 0 ? ~0u : (init_limb<L>(d - 1, 0) << 1);
-        }
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            diag0[l] = init_limb<L>(d0 - 1, l);
-            X[l] = Y[l] = 0;
-        }
-        const int i_top = warp_max(in_dc ? n_w - 1 : -1);
-        // two-column prefetch of the parked row d0-1
-        uint32_t nb1[L], nb2[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) nb1[l] = nb2[l] = ~0u;
-        if (in_dc && d0 > 0) {
-            if (i_top < n_w && i_top >= 0) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) nb1[l] = bnd[(i_top * 32 + lane) * L + l];
-            }
-            if (i_top - 1 < n_w && i_top >= 1) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) nb2[l] = bnd[((i_top - 1) * 32 + lane) * L + l];
-            }
-        }
-        for (int i = i_top; i >= 0; --i) {
-            const bool act = in_dc && i < n_w;
-            const int e = n_w - i - d0;
-            const bool fast = __all_sync(kFull, !act || e >= R + 1);
-            uint32_t north0[L];
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                north0[l] = nb1[l];
-                nb1[l] = nb2[l];
-            }
-            if (in_dc && d0 > 0 && i >= 2 && i - 2 < n_w) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) nb2[l] = bnd[((i - 2) * 32 + lane) * L + l];
-            }
-            if (act) {
-                // text code t_i (non-ACGT -> code 4, all-ones mask)
-                uint32_t w = tw[0];
-#pragma unroll
-                for (int k = 1; k < 2 * L; ++k) w = (i >> 4) == k ? tw[k] : w;
-                int code = static_cast<int>((w >> ((i & 15) * 2)) & 3u);
-                if (hasn) {
-                    uint32_t nwd = tn[0];
-#pragma unroll
-                    for (int k = 1; k < L; ++k) nwd = (i >> 5) == k ? tn[k] : nwd;
-                    if ((nwd >> (i & 31)) & 1u) code = 4;
-                }
-                uint32_t pm[L];
-#pragma unroll
-                for (int l = 0; l < L; ++l) pm[l] = pmv[(code * 32 + lane) * L + l];
-                if (i < C) {
-                    if (fast)
-                        dc_column<L, R, true, true>(col, ic, diag0, north0, pm, e, X, Y);
-                    else
-                        dc_column<L, R, false, true>(col, ic, diag0, north0, pm, e, X, Y);
-                    // fold the column's events into its 2-bit traceback codes:
-                    //   P = X | ~PM, Q = PM & (X | Y)  ->  M=(1,0) S=(1,1) D=(0,1) I=(0,0)
-#pragma unroll
-                    for (int l = 0; l < L; ++l) {
-                        uint32_t* pp = pq + ((i * 2 + 0) * L + l) * 32 + lane;
-                        uint32_t* qp = pq + ((i * 2 + 1) * L + l) * 32 + lane;
-                        const uint32_t pold = d0 > 0 ? *pp : ~pm[l];
-                        const uint32_t qold = d0 > 0 ? *qp : 0u;
-                        *pp = pold | X[l];
-                        *qp = qold | (pm[l] & (X[l] | Y[l]));
-                        X[l] = Y[l] = 0;
-                    }
-                } else {
-                    if (fast)
-                        dc_column<L, R, true, false>(col, ic, diag0, north0, pm, e, X, Y);
-                    else
-                        dc_column<L, R, false, false>(col, ic, diag0, north0, pm, e, X, Y);
-                }
-                // park row d0+R-1 of column i for the next chunk
-#pragma unroll
-                for (int l = 0; l < L; ++l) bnd[(i * 32 + lane) * L + l] = col[R - 1][l];
-            }
-        }
+        const int n_max = warp_max(in_dc ? n_w : 0);
+        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, pmv, txt, pq, bnd, lane);
 
         // ------------------------------------------------ d_opt detection
         bool solved = false;
         if (in_dc) {
-            const int off = WB - m_w;
-            const int r0 = off % L, p0 = off / L;
-            int fr = -1;
-#pragma unroll
-            for (int r = R - 1; r >= 0; --r) {
-                uint32_t v = col[r][0];
-#pragma unroll
-                for (int l = 1; l < L; ++l) v = r0 == l ? col[r][l] : v;
-                if (!((v >> (31 - p0)) & 1u)) fr = r;
-            }
             if (found_d < 0 && fr >= 0) found_d = d0 + fr;
             const bool seg_et = P.et || !first_seg;
             solved = seg_et ? found_d >= 0 : (d0 + R > W);

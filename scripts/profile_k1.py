@@ -1,0 +1,20 @@
+"""Runs K1 on a cfg batch twice (warm-up + profiled launch) for ncu captures."""
+import argparse, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2208_09985_b200 as sg
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cfg", type=int, default=3)
+ap.add_argument("--pairs", type=int, default=100000)
+ap.add_argument("--W", type=int, default=64)
+ap.add_argument("--O", type=int, default=24)
+ap.add_argument("--runs", type=int, default=2)
+a = ap.parse_args()
+batch = sg.synth_packed(a.cfg, 0, a.pairs)
+s = sg.Session(sg.AlignerConfig(W=a.W, O=a.O), batch)
+for _ in range(a.runs):
+    ms, k1 = s.run()
+    print(f"cfg{a.cfg} pairs={a.pairs} K1-K3 {ms:.3f} ms  K1 {k1:.3f} ms  {a.pairs / (ms / 1e3):.0f} aln/s  {s.info()}", flush=True)
+r = s.fetch()
+print("cells_computed", r.total.cells_computed, "ALG_OPS/s (K1)", 4 * ((a.W + 31) // 32) * r.total.cells_computed / (k1 / 1e3) / 1e12, "T")

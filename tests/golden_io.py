@@ -1,0 +1,72 @@
+"""Readers for the reference-generated fixtures in tests/golden/ (see make_golden.py)."""
+from __future__ import annotations
+
+import glob
+import os
+import re
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+COUNTERS = ("stored_bits", "table_writes", "table_reads", "rows_computed", "cells_computed",
+            "rows_possible", "baseline_equiv_bits")
+
+
+def read_golden(name):
+    rows = []
+    with open(os.path.join(HERE, name)) as f:
+        for line in f:
+            parts = line.rstrip("\n").split("\t")
+            hashed = len(parts) == 12
+            r = {"id": parts[0], "distance": int(parts[1])}
+            if hashed:
+                r["hash"], r["runs"] = parts[2], int(parts[3])
+                rest = parts[4:]
+            else:
+                r["cigar"] = parts[2]
+                rest = parts[3:]
+            r["windows"] = int(rest[0])
+            r["counters"] = [int(x) for x in rest[1:8]]
+            rows.append(r)
+    return rows
+
+
+def kat_pairs():
+    out = {}
+    with open(os.path.join(HERE, "kat_pairs.tsv")) as f:
+        for line in f:
+            pid, t, p = line.rstrip("\n").split("\t")
+            out[pid] = (t, p)
+    return out
+
+
+_KAT = re.compile(r"kat_W(\d+)_O(\d+)(?:_s(\d)d(\d)e(\d))?\.tsv$")
+_CFG4 = re.compile(r"cfg4_W(\d+)_O(\d+)(?:_s(\d)d(\d)e(\d))?\.tsv$")
+
+
+def kat_files():
+    """(file, W, O, sene, dent, et) of every KAT result file."""
+    out = []
+    for path in sorted(glob.glob(os.path.join(HERE, "kat_W*.tsv"))):
+        m = _KAT.search(path)
+        s, d, e = (int(m.group(3)), int(m.group(4)), int(m.group(5))) if m.group(3) else (1, 1, 1)
+        out.append((os.path.basename(path), int(m.group(1)), int(m.group(2)), s, d, e))
+    return out
+
+
+def synth_files():
+    """(file, cfg_id, W, O, sene, dent, et) of every synthetic-config file."""
+    out = [("cfg1_full.tsv", 1, 64, 24, 1, 1, 1), ("cfg2_head.tsv", 2, 64, 24, 1, 1, 1),
+           ("cfg3_head.tsv", 3, 64, 24, 1, 1, 1), ("cfg3_tail.tsv", 3, 64, 24, 1, 1, 1),
+           ("cfg5_head.tsv", 5, 64, 24, 1, 1, 1)]
+    for path in sorted(glob.glob(os.path.join(HERE, "cfg4_W*.tsv"))):
+        m = _CFG4.search(path)
+        s, d, e = (int(m.group(3)), int(m.group(4)), int(m.group(5))) if m.group(3) else (1, 1, 1)
+        out.append((os.path.basename(path), 4, int(m.group(1)), int(m.group(2)), s, d, e))
+    return out
+
+
+def pair_index(pid: str) -> int:
+    return int(pid[1:])
+
+
+def run_count(cigar: str) -> int:
+    return len(re.findall(r"\d+[=XID]", cigar))

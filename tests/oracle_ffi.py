@@ -46,7 +46,9 @@ _lib = None
 
 
 def ensure_built() -> None:
-    if not os.path.exists(LIB_PATH):
+    src = [os.path.join(ORACLE_DIR, f) for f in ("genasm_oracle.c", "genasm_oracle.h")]
+    if not os.path.exists(LIB_PATH) or any(os.path.getmtime(f) > os.path.getmtime(LIB_PATH)
+                                           for f in src):
         subprocess.run(["make", "-s", "-C", ORACLE_DIR, "all"], check=True)
 
 
@@ -68,6 +70,11 @@ def lib():
         L.sg_synth_max_pattern.restype = C.c_int64
         L.sg_synth_pair.argtypes = [C.POINTER(SynthSpec), C.c_int64, C.c_char_p,
                                     C.POINTER(C.c_int64), C.c_char_p, C.POINTER(C.c_int64)]
+        L.orc_replay_runs.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.c_void_p,
+                                      C.c_int64]
+        L.orc_replay_runs.restype = C.c_int64
+        L.orc_replay_batch.argtypes = [C.c_int64] + [C.c_void_p] * 9 + [C.c_int]
+        L.orc_replay_batch.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -151,3 +158,16 @@ def fnv1a(s: str) -> str:
     for ch in s.encode():
         h = ((h ^ ch) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     return f"{h:016x}"
+
+
+def replay_batch(codes, results, threads=None) -> int:
+    """Pairs of a CodesBatch whose GPU CIGAR fails validate_replay or whose edit
+    count differs from the reported distance (proj/src/cigar.cpp:70-107)."""
+    import numpy as np
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    dist = np.ascontiguousarray(results.distance, dtype=np.int64)
+    return int(lib().orc_replay_batch(codes.n, ptr(codes.text), ptr(codes.text_off),
+                                      ptr(codes.text_len), ptr(codes.pattern), ptr(codes.pat_off),
+                                      ptr(codes.pat_len), ptr(results.runs),
+                                      ptr(results.cigar_off), ptr(dist),
+                                      threads or (os.cpu_count() or 8)))

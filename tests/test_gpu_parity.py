@@ -1,0 +1,228 @@
+"""Parity of the sm_100a path with the reference (through the C ABI).
+
+* Every golden fixture (produced by the unmodified reference, tests/golden/) is
+  reproduced exactly: distance, CIGAR (or hash + run count), windows and all
+  seven InstrumentationCounters.
+* Random and edge-case pairs at many (W, O, switches) match the oracle
+  restatement (itself pinned to the same fixtures by test_oracle_pin.py).
+* At BASELINE.json's full sizes, size-independent properties hold for every
+  pair: the CIGAR replays text -> pattern (validate_replay,
+  proj/src/cigar.cpp:70-107), its edit count equals the distance, output is
+  deterministic and independent of how pairs are sharded.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import golden_io as G
+import oracle_ffi as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(sg, W, Ov, s=1, d=1, e=1):
+    return sg.AlignerConfig(W=W, O=Ov, sene=bool(s), dent=bool(d), early_termination=bool(e))
+
+
+def _compare(res, k, row):
+    assert int(res.distance[k]) == row["distance"], row["id"]
+    cig = res.cigar_string(k)
+    if "cigar" in row:
+        assert cig == row["cigar"], row["id"]
+    else:
+        assert O.fnv1a(cig) == row["hash"], row["id"]
+        assert G.run_count(cig) == row["runs"], row["id"]
+    assert int(res.windows[k]) == row["windows"], row["id"]
+    assert [int(x) for x in res.counters[k]] == row["counters"], row["id"]
+
+
+@pytest.mark.parametrize("name,W,Ov,s,d,e", G.kat_files())
+def test_reference_kats(gpu, name, W, Ov, s, d, e):
+    sg = gpu
+    pairs = G.kat_pairs()
+    rows = G.read_golden(name)
+    codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
+                                     [sg.encode_sequence(pairs[r["id"]][1]) for r in rows])
+    res = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
+    for k, row in enumerate(rows):
+        _compare(res, k, row)
+
+
+@pytest.mark.parametrize("name,cfg,W,Ov,s,d,e", G.synth_files())
+def test_reference_configs(gpu, name, cfg, W, Ov, s, d, e):
+    sg = gpu
+    rows = G.read_golden(name)
+    first = G.pair_index(rows[0]["id"])
+    assert [G.pair_index(r["id"]) for r in rows] == list(range(first, first + len(rows)))
+    res = sg.align_packed(_cfg(sg, W, Ov, s, d, e), sg.synth_packed(cfg, first, len(rows)))
+    for k, row in enumerate(rows):
+        _compare(res, k, row)
+
+
+def test_reference_doctest_kats(gpu):
+    sg = gpu
+    # proj/tests/test_aligner.cpp:41-48
+    r = sg.align("ACGT", "ACGA", sg.AlignerConfig(W=64, O=33))
+    assert (r.distance, sg.cigar_to_string(r.cigar), r.windows) == (1, "3=1X", 1)
+    # test_aligner.cpp:30-39: identity of a long pair at three window shapes
+    rng = random.Random(41)
+    x = "".join(rng.choice("ACGT") for _ in range(10000))
+    for W, Ov in ((64, 33), (32, 17), (16, 0)):
+        r = sg.align(x, x, sg.AlignerConfig(W=W, O=Ov))
+        assert r.distance == 0 and sg.cigar_to_string(r.cigar) == "10000="
+    # test_dp.cpp:69-75: non-ACGT never matches
+    assert sg.align("ANGT", "ANGT").distance == 1
+    assert sg.align("NNNN", "NNNN").distance == 4
+    # test_aligner.cpp:67-81: per-window counters accumulate exactly
+    y = "".join(rng.choice("ACGT") for _ in range(100))
+    r = sg.align(y, y, sg.AlignerConfig(W=64, O=33, sene=True, dent=False))
+    assert r.windows == 3 and r.distance == 0
+    assert r.counters.rows_computed == 3
+    assert r.counters.stored_bits == 2 * 65 * 64 + 39 * 38
+    assert r.counters.rows_possible == 3 * 65
+
+
+def _rand(rng, n, alphabet="ACGT"):
+    return "".join(rng.choice(alphabet) for _ in range(n))
+
+
+CASES = [(1, 0), (2, 1), (3, 0), (5, 2), (7, 6), (16, 8), (31, 15), (32, 0), (32, 31), (33, 1),
+         (40, 20), (63, 62), (64, 0), (64, 24), (64, 33), (64, 63), (65, 33), (96, 40),
+         (100, 50), (127, 1), (128, 48), (128, 127)]
+
+
+@pytest.mark.parametrize("W,Ov", CASES)
+def test_random_pairs_match_oracle(gpu, W, Ov):
+    """Degenerate and multi-limb windows, N bases, unbalanced and tiny pairs
+    (proj/tests/test_aligner.cpp:163-211, acceptance.cpp:244-254)."""
+    sg = gpu
+    rng = random.Random(W * 1000 + Ov)
+    pairs = []
+    for k in range(24):
+        kind = k % 6
+        if kind == 0:
+            t, p = _rand(rng, rng.randint(1, 300), "ACGTN"), _rand(rng, rng.randint(1, 300), "ACGTN")
+        elif kind == 1:
+            t, p = _rand(rng, rng.randint(200, 700)), _rand(rng, rng.randint(1, 40))
+        elif kind == 2:
+            t, p = _rand(rng, rng.randint(1, 40)), _rand(rng, rng.randint(200, 700))
+        elif kind == 3:
+            t, p = _rand(rng, rng.randint(1, 3)), _rand(rng, rng.randint(1, 3))
+        else:
+            t = _rand(rng, rng.randint(100, 1200))
+            p = list(t[: len(t) - rng.randint(0, 40)])
+            for _ in range(len(p) // 8):
+                pos = rng.randrange(len(p))
+                c = rng.random()
+                if c < 0.4:
+                    p[pos] = rng.choice("ACGTN")
+                elif c < 0.7:
+                    p.insert(pos, rng.choice("ACGT"))
+                elif len(p) > 1:
+                    del p[pos]
+            p = "".join(p)
+        pairs.append((t, p))
+    combos = [(1, 1, 1), (0, 0, 0), (1, 0, 1), (0, 1, 0)]
+    for (s, d, e) in combos:
+        codes = sg.CodesBatch.from_lists([sg.encode_sequence(t) for t, _ in pairs],
+                                         [sg.encode_sequence(p) for _, p in pairs])
+        res = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
+        for k, (t, p) in enumerate(pairs):
+            a = O.align(O.encode(t), O.encode(p), W=W, O=Ov, sene=s, dent=d, et=e)
+            assert int(res.distance[k]) == a.distance, (k, s, d, e)
+            assert res.cigar_string(k) == a.cigar, (k, s, d, e)
+            assert int(res.windows[k]) == a.windows
+            assert [int(x) for x in res.counters[k]] == [a.counters[n] for n in O.COUNTER_NAMES]
+
+
+def test_pairs_within_one_window_are_exact(gpu):
+    """test_aligner.cpp:123-133: max(n, m) <= W is aligned exactly (Levenshtein)."""
+    sg = gpu
+    rng = random.Random(45)
+    pairs = [(_rand(rng, rng.randint(1, 64)), _rand(rng, rng.randint(1, 64))) for _ in range(400)]
+    codes = sg.CodesBatch.from_lists([sg.encode_sequence(t) for t, _ in pairs],
+                                     [sg.encode_sequence(p) for _, p in pairs])
+    res = sg.align_codes(sg.AlignerConfig(W=64, O=33), codes)
+    for k, (t, p) in enumerate(pairs):
+        prev = list(range(len(p) + 1))
+        for i in range(1, len(t) + 1):
+            cur = [i] + [0] * len(p)
+            for j in range(1, len(p) + 1):
+                cur[j] = min(prev[j - 1] + (t[i - 1] != p[j - 1]), prev[j] + 1, cur[j - 1] + 1)
+            prev = cur
+        assert int(res.distance[k]) == prev[-1]
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 5])
+def test_full_size_properties(gpu, cfg_id):
+    """Every pair of the BASELINE config at full size: the CIGAR replays
+    (validate_replay) and its edit count equals the distance; head/tail pairs
+    equal the reference's golden vectors."""
+    sg = gpu
+    codes = sg.synth_codes(cfg_id)
+    res = sg.align_codes(sg.AlignerConfig(W=64, O=24), codes)
+    assert res.n == codes.n
+    assert O.replay_batch(codes, res) == 0
+    assert (res.windows > 0).all()
+    tl, pl = codes.text_len, codes.pat_len
+    assert (res.distance >= np.abs(tl - pl)).all()
+    names = {1: ["cfg1_full.tsv"], 2: ["cfg2_head.tsv"], 3: ["cfg3_head.tsv", "cfg3_tail.tsv"],
+             5: ["cfg5_head.tsv"]}[cfg_id]
+    for name in names:
+        for row in G.read_golden(name):
+            _compare(res, G.pair_index(row["id"]), row)
+
+
+def test_cfg4_full_sweep_properties(gpu):
+    sg = gpu
+    codes = sg.synth_codes(4)
+    pk = sg.pack(codes)
+    for W, Ov in ((32, 12), (64, 24), (64, 33), (128, 48)):
+        res = sg.align_packed(sg.AlignerConfig(W=W, O=Ov), pk)
+        assert O.replay_batch(codes, res) == 0
+        for row in G.read_golden(f"cfg4_W{W}_O{Ov}.tsv"):
+            _compare(res, G.pair_index(row["id"]), row)
+
+
+def test_sharding_and_determinism(gpu):
+    """Output is byte-identical across runs and across shardings of the batch
+    (acceptance.cpp:258-281 checks the same across thread counts)."""
+    sg = gpu
+    pk = sg.synth_packed(5, 0, 3000)
+    cfg = sg.AlignerConfig(W=64, O=24)
+    a = sg.align_packed(cfg, pk)
+    b = sg.align_packed(cfg, pk)
+    c = sg.align_packed(cfg, pk, devices=[0, 0, 0])  # three shards, one device
+    for r in (b, c):
+        assert (r.distance == a.distance).all()
+        assert (r.cigar_off == a.cigar_off).all()
+        assert bytes(r.runs) == bytes(a.runs)
+        assert (r.counters == a.counters).all()
+
+
+def test_session_matches_one_shot(gpu):
+    sg = gpu
+    pk = sg.synth_packed(3, 0, 500)
+    cfg = sg.AlignerConfig(W=64, O=24)
+    one = sg.align_packed(cfg, pk)
+    s = sg.Session(cfg, pk)
+    for _ in range(2):
+        ms, k1 = s.run()
+        assert ms > 0 and 0 < k1 <= ms
+        r = s.fetch()
+        assert (r.distance == one.distance).all() and bytes(r.runs) == bytes(one.runs)
+    s.close()
+
+
+def test_run_batch_api_and_tsv(gpu):
+    import io
+    sg = gpu
+    pairs = [sg.SeqPairRecord("a", "ACGT", "ACGA"), sg.SeqPairRecord("b", "GATTACA", "GATTACA")]
+    br = sg.run_batch(pairs, sg.AlignerConfig(), threads=4)
+    f = io.StringIO()
+    sg.write_batch_tsv(f, pairs, br)
+    assert f.getvalue() == "a\t1\t3=1X\nb\t0\t7=\n"
+    assert br.gpu_launches >= 1 and br.device_ms > 0
+    with pytest.raises(sg.ConfigError):
+        sg.run_batch(pairs, sg.AlignerConfig(), threads=0)
