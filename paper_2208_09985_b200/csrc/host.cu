@@ -565,6 +565,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.O = rc.O;
     p.et = rc.et;
     p.policy = rc.policy;
+    p.two = 2;
     p.distance = st.distance.as<int32_t>();
     p.windows = st.windows.as<int32_t>();
     p.status = st.status.as<int32_t>();

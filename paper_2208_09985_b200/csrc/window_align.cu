@@ -4,24 +4,36 @@
 
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace sgk {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Per limb-count tuning: R rows per register chunk, C traceback-code columns
-// kept in shared memory (>= W-O for the supported O range),
-// WARPS warps per block (warps are independent; blocks only share an SM).
+// Per limb-count tuning: R rows per register chunk (power of two <= 8), C
+// traceback-event columns kept in shared memory (>= W-O for the supported O
+// range, wider windows continue as a new segment), WARPS warps per block
+// (warps are independent; blocks only share an SM).
 template <int L> struct KCfg;
 template <> struct KCfg<1> { static constexpr int R = 8, C = 32, WARPS = 4; };
 template <> struct KCfg<2> { static constexpr int R = 8, C = 40, WARPS = 4; };
 template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
 
+// Shared memory of one warp, in 32-bit words:
+//   txt [WB/8][32] u64   text codes (1 byte per column, 4 = non-ACGT / virtual)
+//   xy  [C+1][2][32][L]  traceback events X / Y per column (column C = dummy)
+//   pm  [5][32][L]       pattern masks per code (code 4: all ones)
+//   sq  [6L+4][32]       packed text (2L+1 words), pattern (2L+1), text N (L+1),
+//                        pattern N (L+1) of the current segment, for traceback
 template <int L> __host__ __device__ constexpr int txt_words() { return (32 * L / 8) * 32 * 2; }
-template <int L> __host__ __device__ constexpr int pq_words() { return KCfg<L>::C * 2 * L * 32; }
+template <int L> __host__ __device__ constexpr int xy_words() {
+    return (KCfg<L>::C + 1) * 2 * 32 * L;
+}
 template <int L> __host__ __device__ constexpr int pm_words() { return 5 * L * 32; }
+template <int L> __host__ __device__ constexpr int sq_words() { return (6 * L + 4) * 32; }
 template <int L> __host__ __device__ constexpr int warp_smem_words() {
-    return txt_words<L>() + pq_words<L>() + pm_words<L>();
+    return txt_words<L>() + xy_words<L>() + pm_words<L>() + sq_words<L>();
 }
 
 // ---------------------------------------------------------------- bit utils
@@ -60,10 +72,11 @@ __device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
     return (b | (b << 7) | (b << 14) | (b << 21)) & 0x01010101u;
 }
 
-// x*2 + b on the FMA pipe (IMAD): the DP shift of limb 0 into limb L-1.
-__device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t b) {
+// x*two + b with `two` a runtime 2: an IMAD on the FMA pipe. With a literal 2
+// ptxas emits LEA, which issues on the ALU pipe the bitvector logic needs.
+__device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t two, uint32_t b) {
     uint32_t r;
-    asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(r) : "r"(x), "r"(b));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(two), "r"(b));
     return r;
 }
 
@@ -150,14 +163,21 @@ __device__ __forceinline__ int warp_max(int v) {
 // One chunk (rows d0..d0+R-1) of GenASM-DC over all columns of a window as a
 // skewed wavefront: at step s row r works on column col0(s) + r, where
 // col0(s) = S0 - s is row 0's column. The R cells of a step are independent
-// (each needs only the previous step's values), which gives the warp R-way
-// instruction-level parallelism instead of an R-long dependency chain.
+// (each needs only the previous step's values), giving R-way instruction-level
+// parallelism instead of an R-long dependency chain per column.
 // Columns >= n_w are "virtual": pattern mask all ones and boundary bits 0,
-// which reproduce the init column R[n][d] exactly, so the fill of the
-// wavefront needs no special code. The pattern masks and the traceback event
-// accumulators of the R columns in flight live in rings indexed by the step
-// at which row 0 entered the column; unrolling the step loop by R makes every
-// ring index static (no register moves).
+// which reproduce the init column R[n][d] exactly, so filling the wavefront
+// needs no special code. The pattern masks and the traceback event
+// accumulators of the R columns in flight live in rings indexed by the step at
+// which row 0 entered the column; unrolling the step loop by R makes every ring
+// index static (no register moves).
+//
+// Cell update (proj/src/dp.cpp:187-211), with c = n - i:
+//   I = shl1(R[i][d-1], [c > d-1]);  D = R[i+1][d-1];  S = shl1(D, [c-1 > d-1])
+//   M = shl1(R[i+1][d], [c-1 > d]) | PM[t_i];   R[i][d] = I & D & S & M
+// S(i, d) equals I(i+1, d) (dp.cpp:193-194 boundary terms coincide), carried
+// in ic. Traceback events of the column:
+//   X |= R & ~shl1(R[i+1][d])  (D(i+1,j+1) < D(i,j));  Y |= R & ~R[i+1][d]  (D(i+1,j) < D(i,j))
 template <int L, int R>
 struct Sweep {
     uint32_t v[R][L];       // latest value of row r (R[col_r][d0 + r])
@@ -167,138 +187,108 @@ struct Sweep {
     uint32_t acc[R][2][L];  // X / Y event ring
 };
 
-// Step U (static) of a group. MODE 0: fast, no capture; 1: fast with capture;
-// 2: slow (explicit boundary bits) with capture. `g` = n_w - S0 - d0 + s; the
-// boundary bits of row r are [g >= 2r] (plus d == 0 for row 0) and [g >= 2r+2]
-// (dp.cpp:187-195 with c = n_w - col: [c > d-1], [c-1 > d]).
-template <int L, int R, int U, int MODE>
+// One cell of row r. bI / bM: boundary bits (0/1).
+template <int L, int R, int SLOT, bool FIRST>
+__device__ __forceinline__ void sweep_cell(Sweep<L, R>& S, int r, const uint32_t (&north)[L],
+                                           uint32_t two, uint32_t bI, uint32_t bM) {
+    uint32_t east[L], diag[L], I[L], M[L], Sv[L], Rv[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        east[l] = S.v[r][l];
+        diag[l] = S.dg[r][l];
+    }
+#pragma unroll
+    for (int l = 0; l + 1 < L; ++l) {
+        I[l] = north[l + 1];
+        M[l] = east[l + 1];
+        Sv[l] = diag[l + 1];
+    }
+    I[L - 1] = dp_shift(north[0], two, bI);
+    M[L - 1] = dp_shift(east[0], two, bM);
+    Sv[L - 1] = S.ic[r];
+#pragma unroll
+    for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | S.pmq[SLOT][l]);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        const uint32_t x = Rv[l] & ~M[l], y = Rv[l] & ~east[l];
+        if (FIRST) {
+            S.acc[SLOT][0][l] = x;
+            S.acc[SLOT][1][l] = y;
+        } else {
+            S.acc[SLOT][0][l] |= x;
+            S.acc[SLOT][1][l] |= y;
+        }
+    }
+    S.ic[r] = I[L - 1];
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        if (r + 1 < R) S.dg[r + 1 < R ? r + 1 : 0][l] = east[l];
+        S.v[r][l] = Rv[l];
+    }
+}
+
+// Rows TOP, TOP-1, ..., TOP-|Rs|+1 of step U (descending: a row reads its
+// north neighbour's value from the previous step before that row updates).
+template <int L, int R, int U, int TOP, int... Rs>
+__device__ __forceinline__ void sweep_rows(Sweep<L, R>& S, const uint32_t (&t)[R + 1],
+                                           uint32_t two, std::integer_sequence<int, Rs...>) {
+    (sweep_cell<L, R, ((U - (TOP - Rs)) & (R - 1)), false>(S, TOP - Rs, S.v[TOP - Rs - 1], two,
+                                                           t[TOP - Rs], t[TOP - Rs + 1]),
+     ...);
+}
+
+// Step U (static) of a group. When `slow` (warp-uniform), the boundary bits
+// come from g = n_w - S0 - d0 + s: row r gets [g >= 2r] (or d == 0) and
+// [g >= 2r + 2] (dp.cpp:187-195 with c = n - i: [c > d-1], [c-1 > d]);
+// otherwise every cell is at least two columns from the edge and both are 1.
+template <int L, int R, int U>
 __device__ __forceinline__ void sweep_step(Sweep<L, R>& S, const uint32_t (&north0)[L],
-                                           const uint32_t (&pm0)[L], int g, bool z0) {
+                                           const uint32_t (&pm0)[L], uint32_t two, uint32_t one,
+                                           int g, bool z0, bool slow) {
 #pragma unroll
     for (int l = 0; l < L; ++l) S.pmq[U][l] = pm0[l];
     uint32_t t[R + 1];
-    if (MODE == 2) {
+    if (slow) {
 #pragma unroll
         for (int k = 0; k <= R; ++k) t[k] = static_cast<uint32_t>(g >= 2 * k);
         t[0] |= static_cast<uint32_t>(z0);
+    } else {
+#pragma unroll
+        for (int k = 0; k <= R; ++k) t[k] = one;
     }
-#pragma unroll
-    for (int r = R - 1; r >= 0; --r) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int slot = (U - r) & (R - 1);
-        uint32_t north[L], east[L], diag[L], pm[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            north[l] = r == 0 ? north0[l] : S.v[r == 0 ? 0 : r - 1][l];
-            east[l] = S.v[r][l];
-            diag[l] = S.dg[r][l];
-            pm[l] = S.pmq[slot][l];
-        }
-        const uint32_t bI = MODE == 2 ? t[r] : 1u;
-        const uint32_t bM = MODE == 2 ? t[r + 1] : 1u;
-        uint32_t I[L], M[L], Sv[L], Rv[L];
-#pragma unroll
-        for (int l = 0; l + 1 < L; ++l) {
-            I[l] = north[l + 1];
-            M[l] = east[l + 1];
-            Sv[l] = diag[l + 1];
-        }
-        I[L - 1] = dp_shift(north[0], bI);
-        M[L - 1] = dp_shift(east[0], bM);
-        Sv[L - 1] = S.ic[r];
-#pragma unroll
-        for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | pm[l]);
-        if (MODE != 0) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                const uint32_t x = Rv[l] & ~M[l], y = Rv[l] & ~east[l];
-                if (r == 0) {
-                    S.acc[slot][0][l] = x;
-                    S.acc[slot][1][l] = y;
-                } else {
-                    S.acc[slot][0][l] |= x;
-                    S.acc[slot][1][l] |= y;
-                }
-            }
-        }
-        S.ic[r] = I[L - 1];
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            if (r + 1 < R) S.dg[r + 1 < R ? r + 1 : 0][l] = east[l];
-            S.v[r][l] = Rv[l];
-        }
-    }
+    sweep_rows<L, R, U, R - 1>(S, t, two, std::make_integer_sequence<int, R - 1>{});
+    sweep_cell<L, R, U, true>(S, 0, north0, two, t[0], t[1]);
 #pragma unroll
     for (int l = 0; l < L; ++l) S.dg[0][l] = north0[l];
 }
 
-// Drain step K (1..R-1, static): row 0's column is -K; rows r >= K finish
-// columns r-K. Boundary bits explicit (MODE 2 rule).
-template <int L, int R, int K>
-__device__ __forceinline__ void drain_step(Sweep<L, R>& S, int g) {
-    uint32_t t[R + 1];
-#pragma unroll
-    for (int k = 0; k <= R; ++k) t[k] = static_cast<uint32_t>(g >= 2 * k);
-#pragma unroll
-    for (int r = R - 1; r >= K; --r) {
-        const int slot = (R - 1 + K - r) & (R - 1);
-        uint32_t north[L], east[L], diag[L], pm[L];
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            north[l] = S.v[r - 1][l];
-            east[l] = S.v[r][l];
-            diag[l] = S.dg[r][l];
-            pm[l] = S.pmq[slot][l];
-        }
-        uint32_t I[L], M[L], Sv[L], Rv[L];
-#pragma unroll
-        for (int l = 0; l + 1 < L; ++l) {
-            I[l] = north[l + 1];
-            M[l] = east[l + 1];
-            Sv[l] = diag[l + 1];
-        }
-        I[L - 1] = dp_shift(north[0], t[r]);
-        M[L - 1] = dp_shift(east[0], t[r + 1]);
-        Sv[L - 1] = S.ic[r];
-#pragma unroll
-        for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | pm[l]);
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            S.acc[slot][0][l] |= Rv[l] & ~M[l];
-            S.acc[slot][1][l] |= Rv[l] & ~east[l];
-        }
-        S.ic[r] = I[L - 1];
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            if (r + 1 < R) S.dg[r + 1 < R ? r + 1 : 0][l] = east[l];
-            S.v[r][l] = Rv[l];
-        }
-    }
-}
-
 // Side effects of the column row R-1 just finished (static ring SLOT): park
-// its value for the next chunk and fold the column's events into the 2-bit
-// traceback codes P = X | ~PM, Q = PM & (X | Y)  (M=(1,0) S=(1,1) D=(0,1) I=(0,0)).
-template <int L, int R, int C, int SLOT, bool CAP>
-__device__ __forceinline__ void finish_col(const Sweep<L, R>& S, int colf, int n_w, int d0,
-                                           uint32_t* __restrict__ pq, uint32_t* __restrict__ bnd,
+// its value for the next chunk, store the column's events (OR-ed into the
+// earlier chunks' events). Out-of-range columns go to the dummy slots.
+template <int L, int R, int C, int SLOT>
+__device__ __forceinline__ void finish_col(const Sweep<L, R>& S, int colf, int n_w,
+                                           bool any_parked, uint32_t keep_old,
+                                           uint32_t* __restrict__ xy, uint32_t* __restrict__ bnd,
                                            int lane) {
-    if (colf >= 0 && colf < n_w) {
+    constexpr int WB = 32 * L;
+    const bool real = colf >= 0 && colf < n_w;
+    const int cb = real ? colf + 2 : WB + 2;
+    const int cx = real && colf < C ? colf : C;
 #pragma unroll
-        for (int l = 0; l < L; ++l) bnd[(colf * 32 + lane) * L + l] = S.v[R - 1][l];
-        if (CAP && colf < C) {
+    for (int l = 0; l < L; ++l) bnd[(cb * 32 + lane) * L + l] = S.v[R - 1][l];
+    uint32_t* px = xy + ((cx * 2 + 0) * 32 + lane) * L;
+    uint32_t* py = xy + ((cx * 2 + 1) * 32 + lane) * L;
+    if (any_parked) {  // warp-uniform: some lane is past its first chunk
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                uint32_t* pp = pq + ((colf * 2 + 0) * L + l) * 32 + lane;
-                uint32_t* qp = pq + ((colf * 2 + 1) * L + l) * 32 + lane;
-                const uint32_t pm = S.pmq[SLOT][l];
-                const uint32_t x = S.acc[SLOT][0][l], y = S.acc[SLOT][1][l];
-                const uint32_t pold = d0 > 0 ? *pp : ~pm;
-                const uint32_t qold = d0 > 0 ? *qp : 0u;
-                *pp = pold | x;
-                *qp = qold | (pm & (x | y));
-            }
+        for (int l = 0; l < L; ++l) {
+            px[l] = (px[l] & keep_old) | S.acc[SLOT][0][l];
+            py[l] = (py[l] & keep_old) | S.acc[SLOT][1][l];
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            px[l] = S.acc[SLOT][0][l];
+            py[l] = S.acc[SLOT][1][l];
         }
     }
 }
@@ -312,42 +302,58 @@ __device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0,
     return (v >> (31 - p0)) & 1u;
 }
 
-template <int L, int R, int C, int MODE>
-__device__ __forceinline__ void sweep_group(Sweep<L, R>& S, const uint32_t (&nb)[R][L],
+// Parked-row layout (per lane): slot c + 2 holds column c (slots 0 and 1 pad
+// the two-step-ahead prefetch past column 0), slot WB + 2 is the dummy store
+// target for virtual columns, slot WB + 3 holds R[n][d0 - 1] for first chunks.
+template <int L> __device__ __forceinline__ int bslot(int col) { return col + 2; }
+
+// One group of R steps (static ring slots). `drain` (warp-uniform) marks the
+// group after row 0 reached column 0: rows 1..R-1 finish their last columns
+// (rows already past column 0 compute harmless values on negative columns)
+// and each row's bit j = 0 at column 0 is tested as it gets there.
+template <int L, int R, int C>
+__device__ __forceinline__ void sweep_group(Sweep<L, R>& S, uint32_t (&nbr)[2][L],
+                                            const uint32_t* __restrict__ nbp, int nstride,
                                             uint64_t codes8, int col_top,
-                                            const uint32_t* __restrict__ pmv, int g0, bool z0,
-                                            int n_w, int d0, uint32_t* __restrict__ pq,
-                                            uint32_t* __restrict__ bnd, int lane) {
-#define SG_STEP(U)                                                                          \
-    if ((U) < R) {                                                                          \
-        const int col0 = col_top - (U);                                                     \
-        const int code = static_cast<int>((codes8 >> (8 * (col0 & 7))) & 0xFFu);            \
-        uint32_t pm0[L];                                                                    \
-        _Pragma("unroll") for (int l = 0; l < L; ++l) pm0[l] = pmv[(code * 32 + lane) * L + l]; \
-        sweep_step<L, R, ((U) < R ? (U) : 0), MODE>(S, nb[(U) < R ? (U) : 0], pm0, g0 + (U), z0); \
-        finish_col<L, R, C, (((U) + 1) & (R - 1)), MODE != 0>(S, col0 + R - 1, n_w, d0, pq, bnd, \
-                                                            lane);                           \
+                                            const uint32_t* __restrict__ pmv, uint32_t two,
+                                            uint32_t one, int g0, bool z0, bool slow, bool drain,
+                                            int n_w, bool any_parked, uint32_t keep_old,
+                                            uint32_t* __restrict__ xy,
+                                            uint32_t* __restrict__ bnd, int lane, int r0,
+                                            int p0, int& fr) {
+#define SG_STEP(U)                                                                           \
+    if ((U) < R) {                                                                           \
+        constexpr int UU = (U) < R ? (U) : 0;                                                \
+        const int col0 = col_top - UU;                                                       \
+        int code = static_cast<int>((codes8 >> (8 * (col0 & 7))) & 0xFFu);                   \
+        code = col0 >= 0 && col0 < n_w ? code : 4; /* virtual column: all-ones mask */       \
+        uint32_t pm0[L], north0[L];                                                          \
+        _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
+            pm0[l] = pmv[(code * 32 + lane) * L + l];                                        \
+            north0[l] = nbr[UU & 1][l];                                                      \
+        }                                                                                    \
+        /* prefetch the parked row for step UU + 2 (two steps of latency hiding) */          \
+        const uint32_t* src = nbp - (UU + 2) * nstride;                                      \
+        _Pragma("unroll") for (int l = 0; l < L; ++l) nbr[UU & 1][l] = src[l];               \
+        if (!drain || UU + 1 < R) {                                                          \
+            sweep_step<L, R, UU>(S, north0, pm0, two, one, g0 + UU, z0, slow);               \
+            finish_col<L, R, C, ((UU + 1) & (R - 1))>(S, col0 + R - 1, n_w, any_parked,     \
+                                                       keep_old, xy, bnd, lane);             \
+            if (drain && fr < 0 && UU + 1 < R && !top_bit<L, R>(S, UU + 1, r0, p0))          \
+                fr = UU + 1;                                                                 \
+        }                                                                                    \
     }
     SG_STEP(0) SG_STEP(1) SG_STEP(2) SG_STEP(3) SG_STEP(4) SG_STEP(5) SG_STEP(6) SG_STEP(7)
 #undef SG_STEP
 }
 
-template <int L, int R, int C, int K>
-__device__ __forceinline__ void drain_one(Sweep<L, R>& S, int g, int n_w, int d0, uint32_t* pq,
-                                          uint32_t* bnd, int lane, int r0, int p0, int& fr) {
-    if (K < R) {
-        drain_step<L, R, (K < R ? K : 1)>(S, g);
-        finish_col<L, R, C, (K & (R - 1)), true>(S, R - 1 - K, n_w, d0, pq, bnd, lane);
-        if (fr < 0 && !top_bit<L, R>(S, K < R ? K : 0, r0, p0)) fr = K;
-    }
-}
-
-// One chunk of rows d0..d0+R-1 over columns n_w-1..0 (n_w = 0: inactive lane).
+// One chunk of rows d0..d0+R-1 over columns n_w-1..0 (n_w = 0: idle lane).
 // Returns the first row r of the chunk with bit j=0 of R[0][d0+r] clear, or -1.
 template <int L, int R, int C>
-__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max,
+__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, bool any_parked,
+                                        uint32_t two, uint32_t one,
                                         const uint32_t* __restrict__ pmv,
-                                        const uint64_t* __restrict__ txt, uint32_t* __restrict__ pq,
+                                        const uint64_t* __restrict__ txt, uint32_t* __restrict__ xy,
                                         uint32_t* __restrict__ bnd, int lane) {
     constexpr int WB = 32 * L;
     static_assert((R & (R - 1)) == 0 && R <= 8 && WB % R == 0, "R must be a power of two <= 8");
@@ -368,50 +374,40 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max,
     const int tsteps = ((n_max + R - 1) / R) * R;
     const int S0 = tsteps - 1;
     const bool z0 = d0 == 0;
-    uint32_t init_north[L];
+    const uint32_t keep_old = d0 > 0 ? ~0u : 0u;
+    // Row-0 north inputs: the parked row d0-1. First chunks read R[n][-1] from
+    // slot WB+3 (stride 0); virtual columns >= n_w hold R[n][d0-1] (filled here).
+    uint32_t* const init_slot = bnd + ((WB + 3) * 32 + lane) * L;
 #pragma unroll
-    for (int l = 0; l < L; ++l) init_north[l] = init_limb<L>(d0 - 1, l);
-    // row-0 north inputs (the parked row d0-1), prefetched one group ahead
-    uint32_t nb[R][L], nbn[R][L];
-    auto fetch_nb = [&](uint32_t (&dst)[R][L], int col_top) {
-#pragma unroll
-        for (int u = 0; u < R; ++u) {
-            const int col = col_top - u;
-            const bool real = col >= 0 && col < n_w && d0 > 0;
+    for (int l = 0; l < L; ++l) init_slot[l] = init_limb<L>(d0 - 1, l);
+    if (d0 > 0)
+        for (int c = n_w; c <= S0; ++c)
 #pragma unroll
             for (int l = 0; l < L; ++l)
-                dst[u][l] = real ? bnd[(col * 32 + lane) * L + l] : init_north[l];
-        }
-    };
-    fetch_nb(nb, S0);
-    for (int sg = 0; sg < tsteps; sg += R) {
-        const int col_top = S0 - sg;
-        if (sg + R < tsteps) fetch_nb(nbn, col_top - R);
-        const uint64_t codes8 = txt[(col_top >> 3) * 32 + lane];
-        const int g0 = n_w - S0 - d0 + sg;
-        const bool slow = __any_sync(kFull, n_w > 0 && g0 < 2 * R);
-        if (slow)
-            sweep_group<L, R, C, 2>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
-        else if (col_top - R + 1 < C)
-            sweep_group<L, R, C, 1>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
-        else
-            sweep_group<L, R, C, 0>(S, nb, codes8, col_top, pmv, g0, z0, n_w, d0, pq, bnd, lane);
+                bnd[(bslot<L>(c) * 32 + lane) * L + l] = init_limb<L>(d0 - 1, l);
+    const int nstride = d0 > 0 ? 32 * L : 0;
+    const uint32_t* nbp0 = d0 > 0 ? bnd + (bslot<L>(S0) * 32 + lane) * L : init_slot;
+    uint32_t nbr[2][L];
 #pragma unroll
-        for (int u = 0; u < R; ++u)
-#pragma unroll
-            for (int l = 0; l < L; ++l) nb[u][l] = nbn[u][l];
+    for (int l = 0; l < L; ++l) {
+        nbr[0][l] = nbp0[l];
+        nbr[1][l] = nbp0[l - nstride];
     }
     const int off = WB - m_w;
     const int r0 = off % L, p0 = off / L;
-    int fr = top_bit<L, R>(S, 0, r0, p0) ? -1 : 0;
-    const int gd = n_w - S0 - d0 + tsteps;  // g at drain step 1 minus 1
-    drain_one<L, R, C, 1>(S, gd + 0, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 2>(S, gd + 1, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 3>(S, gd + 2, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 4>(S, gd + 3, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 5>(S, gd + 4, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 6>(S, gd + 5, n_w, d0, pq, bnd, lane, r0, p0, fr);
-    drain_one<L, R, C, 7>(S, gd + 6, n_w, d0, pq, bnd, lane, r0, p0, fr);
+    int fr = -1;
+    for (int sg = 0; sg <= tsteps; sg += R) {
+        const bool drain = sg == tsteps;  // the extra group: rows 1..R-1 finish
+        const int col_top = S0 - sg;
+        const uint32_t* nbp = drain ? init_slot : nbp0 - sg * nstride;
+        const uint64_t codes8 = txt[((col_top < 0 ? 0 : col_top) >> 3) * 32 + lane];
+        const int g0 = n_w - S0 - d0 + sg;
+        const bool slow = drain || __any_sync(kFull, n_w > 0 && g0 < 2 * R);
+        if (drain && !top_bit<L, R>(S, 0, r0, p0)) fr = 0;  // row 0 just left column 0
+        sweep_group<L, R, C>(S, nbr, nbp, drain ? 0 : nstride, codes8, col_top, pmv, two, one,
+                             g0, z0, slow, drain, n_w, any_parked, keep_old, xy, bnd, lane, r0,
+                             p0, fr);
+    }
     return fr;
 }
 
@@ -420,18 +416,27 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max,
 template <int L>
 __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     k1_window_align(const AlignParams P) {
-    constexpr int R = KCfg<L>::R, C = KCfg<L>::C, WB = 32 * L;
+    constexpr int R = KCfg<L>::R, C = KCfg<L>::C, WB = 32 * L, NW = 2 * L;
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    uint64_t* const txt = reinterpret_cast<uint64_t*>(smem + wib * warp_smem_words<L>());
-    uint32_t* const pq = smem + wib * warp_smem_words<L>() + txt_words<L>();  // [C][2][L][32]
-    uint32_t* const pmv = pq + pq_words<L>();                                 // [5][32][L]
+    uint32_t* const wbase = smem + wib * warp_smem_words<L>();
+    uint64_t* const txt = reinterpret_cast<uint64_t*>(wbase);   // [WB/8][32]
+    uint32_t* const xy = wbase + txt_words<L>();                 // [C+1][2][32][L]
+    uint32_t* const pmv = xy + xy_words<L>();                    // [5][32][L]
+    uint32_t* const sq = pmv + pm_words<L>();                    // [6L+4][32]
+    uint32_t* const sq_t = sq;                                   // text words   (NW+1)
+    uint32_t* const sq_p = sq + (NW + 1) * 32;                   // pattern words (NW+1)
+    uint32_t* const sq_tn = sq + (2 * NW + 2) * 32;              // text N words (L+1)
+    uint32_t* const sq_pn = sq + (2 * NW + 3 + L) * 32;          // pattern N words (L+1)
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
-    uint32_t* const bnd = P.bnd + gwarp * (WB + 1) * 32 * L;  // [WB+1][32][L]
+    uint32_t* const bnd = P.bnd + gwarp * (WB + 4) * 32 * L;    // [WB+4][32][L]
+    const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
 
 #pragma unroll
     for (int l = 0; l < L; ++l) pmv[(4 * 32 + lane) * L + l] = ~0u;  // non-ACGT text
+#pragma unroll
+    for (int b = 0; b < WB / 8; ++b) txt[b * 32 + lane] = 0x0404040404040404ull;  // idle lanes
 
     const int W = P.W;
     const int step_limit = W - P.O;
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     bool first_seg = true;
     int d0 = 0, found_d = -1, expect_d = -1;
     int dist = 0, nwin = 0, status = 0;
-    long long window_cap = 0;
+    int window_cap = 0;
     // output
     uint32_t* outw = nullptr;
     int out_bytes = 0, cur_op = -1, acc_n = 0;
@@ -455,92 +460,102 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     unsigned long long c_stored = 0, c_writes = 0, c_reads = 0, c_rows = 0, c_cells = 0,
                        c_bequiv = 0;
 
-    auto put_byte = [&](uint32_t b) {
-        acc |= b << (8 * acc_n);
-        ++out_bytes;
-        if (++acc_n == 4) {
-            *outw++ = acc;
-            acc = 0;
-            acc_n = 0;
-        }
-    };
-    auto flush_run = [&]() {
-        if (cur_op < 0) return;
-        long long len = cur_len;
-        const uint32_t hi = static_cast<uint32_t>(cur_op) << 6;
-        while (len > 64) {
-            put_byte(hi | 63u);
-            len -= 64;
-        }
-        put_byte(hi | static_cast<uint32_t>(len - 1));
-        cur_op = -1;
-        cur_len = 0;
-    };
-    auto emit = [&](int op, long long len) {  // cigar_append, proj/src/cigar.cpp:9-16
+    // CIGAR runs (cigar_append, proj/src/cigar.cpp:9-16): the open run is
+    // (cur_op, cur_len); a run closed by an op change waits in (pend_op,
+    // pend_len) until the single writer below emits it as bytes
+    // (op << 6) | (len - 1), len 1..64 per byte.
+    int pend_op = -1;
+    long long pend_len = 0;
+    auto emit = [&](int op, long long len) {
         if (op == cur_op) {
             cur_len += len;
         } else {
-            flush_run();
+            pend_op = cur_op;
+            pend_len = cur_len;
             cur_op = op;
             cur_len = len;
         }
     };
+    auto write_pending = [&]() {
+        while (pend_op >= 0) {
+            const long long piece = pend_len > 64 ? 64 : pend_len;
+            acc |= ((static_cast<uint32_t>(pend_op) << 6) | static_cast<uint32_t>(piece - 1))
+                   << (8 * acc_n);
+            ++out_bytes;
+            if (++acc_n == 4) {
+                *outw++ = acc;
+                acc = 0;
+                acc_n = 0;
+            }
+            pend_len -= piece;
+            if (pend_len == 0) pend_op = -1;
+        }
+    };
 
-    // Pattern masks and text codes of the current segment.
+    // Pattern masks, text codes and packed sequences of the current segment.
     auto load_segment = [&]() {
         const int off = WB - m_w;
-        uint32_t pw[2 * L];
-        load_codes<2 * L>(P.seq, pbase + poff, pw);
-        uint32_t pn[L];
+        uint32_t pw[NW + 1], pn[L + 1], tw[NW + 1], tn[L + 1];
+        load_codes<NW + 1>(P.seq, pbase + poff, pw);
+        load_codes<NW + 1>(P.seq, tbase + toff, tw);
 #pragma unroll
-        for (int l = 0; l < L; ++l) pn[l] = 0;
-        if (hasn) load_bits<L>(P.nmask, pbase + poff, pn);
+        for (int l = 0; l <= L; ++l) pn[l] = tn[l] = 0;
+        if (hasn) {
+            load_bits<L + 1>(P.nmask, pbase + poff, pn);
+            load_bits<L + 1>(P.nmask, tbase + toff, tn);
+        }
+        uint32_t pwl[NW], pnl[L];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) pwl[k] = pw[k];
+#pragma unroll
+        for (int k = 0; k < L; ++k) pnl[k] = pn[k];
 #pragma unroll
         for (int r = 0; r < L; ++r) {
             const int rho = class_of<L>(r, off);
-            const uint32_t lo = limbify<L>(gather_codes<L>(pw, rho, 0), r, off, rho);
-            const uint32_t hi = limbify<L>(gather_codes<L>(pw, rho, 1), r, off, rho);
-            const uint32_t nn = hasn ? limbify<L>(gather_bits<L>(pn, rho), r, off, rho) : 0u;
+            const uint32_t lo = limbify<L>(gather_codes<L>(pwl, rho, 0), r, off, rho);
+            const uint32_t hi = limbify<L>(gather_codes<L>(pwl, rho, 1), r, off, rho);
+            const uint32_t nn = hasn ? limbify<L>(gather_bits<L>(pnl, rho), r, off, rho) : 0u;
             // PM[c] bit = 0 iff pattern base == c (proj/src/dp.cpp:8-21); N matches nothing
             pmv[(0 * 32 + lane) * L + r] = lo | hi | nn;
             pmv[(1 * 32 + lane) * L + r] = ~lo | hi | nn;
             pmv[(2 * 32 + lane) * L + r] = lo | ~hi | nn;
             pmv[(3 * 32 + lane) * L + r] = ~lo | ~hi | nn;
         }
-        uint32_t tw[2 * L], tn[L];
-        load_codes<2 * L>(P.seq, tbase + toff, tw);
+        // text codes as bytes, 8 columns per u64 (non-ACGT -> 4); columns >= n_w
+        // are mapped to code 4 by the sweep itself
+        uint32_t* const txt32 = reinterpret_cast<uint32_t*>(txt);
 #pragma unroll
-        for (int l = 0; l < L; ++l) tn[l] = 0;
-        if (hasn) load_bits<L>(P.nmask, tbase + toff, tn);
-        // text codes as bytes, 8 columns per u64; non-ACGT and columns >= n_w -> 4
+        for (int h = 0; h < WB / 4; ++h) {  // 4 columns per 32-bit half
+            uint32_t c = spread4(tw[h >> 2] >> (8 * (h & 3)));
+            if (hasn) {
+                const uint32_t nm = spread4bits(tn[h >> 3] >> (4 * (h & 7))) * 0xFFu;
+                c = (c & ~nm) | (0x04040404u & nm);
+            }
+            txt32[((h >> 1) * 32 + lane) * 2 + (h & 1)] = c;
+        }
+        // packed sequences for the traceback's match runs
 #pragma unroll
-        for (int b = 0; b < WB / 8; ++b) {
-            const uint32_t x = (tw[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
-            uint64_t c = static_cast<uint64_t>(spread4(x)) |
-                         (static_cast<uint64_t>(spread4(x >> 8)) << 32);
-            const uint32_t nb8 = (tn[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-            uint64_t m = (static_cast<uint64_t>(spread4bits(nb8)) |
-                          (static_cast<uint64_t>(spread4bits(nb8 >> 4)) << 32)) * 0xFFull;
-            const int valid = n_w - 8 * b;
-            if (valid < 8) m |= valid <= 0 ? ~0ull : (~0ull << (8 * valid));
-            c = (c & ~m) | (0x0404040404040404ull & m);
-            txt[b * 32 + lane] = c;
+        for (int k = 0; k <= NW; ++k) {
+            sq_t[k * 32 + lane] = tw[k];
+            sq_p[k * 32 + lane] = pw[k];
+        }
+#pragma unroll
+        for (int k = 0; k <= L; ++k) {
+            sq_tn[k * 32 + lane] = tn[k];
+            sq_pn[k * 32 + lane] = pn[k];
         }
     };
 
-    // Sets up the next logical window of the current pair (aligner.cpp:44-64).
-    // Returns false when the pair is complete (residues appended).
+    // Geometry of the next logical window of the current pair
+    // (aligner.cpp:44-64). Returns false when the pair is complete (residues
+    // appended).
     auto next_window = [&]() -> bool {
         const int n_rem = n_tot - toff, m_rem = m_tot - poff;
-        if (n_rem == 0 && m_rem == 0) return false;
-        if (n_rem == 0) {
-            emit(2, m_rem);
-            dist += m_rem;
-            return false;
-        }
-        if (m_rem == 0) {
-            emit(3, n_rem);
-            dist += n_rem;
+        if (n_rem == 0 || m_rem == 0) {
+            if (n_rem + m_rem > 0) {  // aligner.cpp:48-57
+                emit(n_rem == 0 ? 2 : 3, n_rem + m_rem);
+                dist += n_rem + m_rem;
+            }
             return false;
         }
         const bool fin = n_rem <= W && m_rem <= W;
@@ -551,12 +566,14 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         d0 = 0;
         found_d = -1;
         expect_d = -1;
-        load_segment();
         return true;
     };
 
     auto finish_pair = [&]() {
-        flush_run();
+        write_pending();
+        pend_op = cur_op;
+        pend_len = cur_len;
+        write_pending();
         if (acc_n) *outw = acc;
         P.distance[pair] = dist;
         P.windows[pair] = nwin;
@@ -574,7 +591,14 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         }
     };
 
-    auto start_pair = [&](int q) {
+    // Claim the next pair for the calling (possibly divergent) lanes.
+    auto fetch = [&]() {
+        const unsigned active = __activemask();
+        const int leader = __ffs(active) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(P.next_pair, static_cast<unsigned>(__popc(active)));
+        base = __shfl_sync(active, base, leader);
+        const int q = static_cast<int>(base + __popc(active & ((1u << lane) - 1u)));
         pair = q < P.n_pairs ? (P.order ? P.order[q] : q) : -1;
         if (pair < 0) return;
         n_tot = P.text_len[pair];
@@ -584,40 +608,69 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         hasn = P.has_n ? P.has_n[pair] != 0 : false;
         toff = poff = 0;
         dist = nwin = status = 0;
-        window_cap = 4ll * ((static_cast<long long>(n_tot) + m_tot) / step_limit + 2);
+        window_cap = 4 * ((n_tot + m_tot) / step_limit + 2);  // aligner.cpp:40
         outw = P.scratch + (P.bound_off[pair] >> 2);
         out_bytes = 0;
-        cur_op = -1;
-        cur_len = 0;
+        cur_op = pend_op = -1;
+        cur_len = pend_len = 0;
         acc = 0;
         acc_n = 0;
         c_stored = c_writes = c_reads = c_rows = c_cells = c_bequiv = 0;
     };
 
-    // Claim the next pair(s) for the calling (possibly divergent) lanes.
-    auto fetch = [&]() {
-        const unsigned active = __activemask();
-        const int leader = __ffs(active) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(P.next_pair, static_cast<unsigned>(__popc(active)));
-        base = __shfl_sync(active, base, leader);
-        const int q = static_cast<int>(base + __popc(active & ((1u << lane) - 1u)));
-        start_pair(q);
+    // Matching bases from (i, j) on (0..16; 0 at a mismatch or a non-ACGT base).
+    auto match_run = [&](int i, int j) -> int {
+        const int wi = i >> 4, si = 2 * (i & 15), wj = j >> 4, sj = 2 * (j & 15);
+        const uint32_t t = __funnelshift_r(sq_t[wi * 32 + lane], sq_t[(wi + 1) * 32 + lane], si);
+        const uint32_t p = __funnelshift_r(sq_p[wj * 32 + lane], sq_p[(wj + 1) * 32 + lane], sj);
+        uint32_t x = t ^ p;
+        x = (x | (x >> 1)) & 0x55555555u;  // bit 2k: base k differs
+        if (hasn) {
+            const uint32_t tn = __funnelshift_r(sq_tn[(i >> 5) * 32 + lane],
+                                                sq_tn[((i >> 5) + 1) * 32 + lane], i & 31);
+            const uint32_t pn = __funnelshift_r(sq_pn[(j >> 5) * 32 + lane],
+                                                sq_pn[((j >> 5) + 1) * 32 + lane], j & 31);
+            uint32_t s = (tn | pn) & 0xFFFFu;  // bit k: base k is non-ACGT -> even bit 2k
+            s = (s | (s << 8)) & 0x00FF00FFu;
+            s = (s | (s << 4)) & 0x0F0F0F0Fu;
+            s = (s | (s << 2)) & 0x33333333u;
+            s = (s | (s << 1)) & 0x55555555u;
+            x |= s;
+        }
+        return x ? (__ffs(x) - 1) >> 1 : 16;
     };
 
-    fetch();
-    while (pair >= 0 && !next_window()) {  // cannot happen for valid pairs (n, m >= 1)
-        finish_pair();
-        fetch();
-    }
-
+    bool need_pair = true, need_window = false, need_load = false;
     for (;;) {
+        // ---------------------------------------------- per-lane setup
+        while (need_pair || need_window) {
+            if (need_pair) {
+                fetch();
+                need_pair = false;
+                if (pair < 0) break;
+                need_window = true;
+            }
+            if (status == 0 && next_window()) {
+                need_load = true;
+            } else {
+                finish_pair();
+                pair = -1;
+                need_pair = true;
+            }
+            need_window = false;
+        }
+        if (need_load) {
+            load_segment();
+            need_load = false;
+        }
         const bool in_dc = pair >= 0;
         if (!__any_sync(kFull, in_dc)) break;
 
         // ------------------------------------------------ DC: one chunk
         const int n_max = warp_max(in_dc ? n_w : 0);
-        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, pmv, txt, pq, bnd, lane);
+        const bool any_parked = __any_sync(kFull, in_dc && d0 > 0);
+        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, any_parked, two, one,
+                                         pmv, txt, xy, bnd, lane);
 
         // ------------------------------------------------ d_opt detection
         bool solved = false;
@@ -650,43 +703,49 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
             } else if (found_d != expect_d) {
                 status = kStInternal | kDetSegment;
             }
-            // GenASM-TB (traceback.cpp:56-113) over the 2-bit codes
+            // GenASM-TB (traceback.cpp:56-113). On the path D(i,j) == d, so
+            // Match <=> t_i == p_j (both ACGT) and runs of matches are taken
+            // at once; at a mismatch the events pick Sub > Del > Ins.
             const int off = WB - m_w;
             int i = 0, j = 0, d = found_d < 0 ? 0 : found_d, steps = 0;
+            const int lim = limit >= 0 ? limit : 0x3FFFFFFF;
             bool cont = false;
             for (;;) {
-                if (limit >= 0 && steps == limit) break;
-                if (i == n_w && j == m_w) break;
-                int op;
-                if (i == n_w) {
-                    if (d != m_w - j) status = kStInternal | kDetBudgetI;
-                    op = 2;
-                } else if (j == m_w) {
-                    if (d != n_w - i) status = kStInternal | kDetBudgetD;
-                    op = 3;
+                const int rem = lim - steps;
+                if (rem == 0 || (i == n_w && j == m_w)) break;
+                int op, k;
+                if (i == n_w || j == m_w) {  // one side consumed: the budget is indels
+                    op = i == n_w ? 2 : 3;
+                    const int left = i == n_w ? m_w - j : n_w - i;
+                    if (d != left) status = kStInternal | (i == n_w ? kDetBudgetI : kDetBudgetD);
+                    k = min(rem, left);
                 } else if (i >= C) {
                     cont = true;
                     break;
                 } else {
-                    c_reads += d == 0 ? 1 : 3;
-                    const int q = j + off;
-                    const int r = q % L, p = q / L;
-                    const uint32_t pw = pq[((i * 2 + 0) * L + r) * 32 + lane];
-                    const uint32_t qw = pq[((i * 2 + 1) * L + r) * 32 + lane];
-                    const int pb = static_cast<int>((pw >> (31 - p)) & 1u);
-                    const int qb = static_cast<int>((qw >> (31 - p)) & 1u);
-                    op = qb | ((pb ^ 1) << 1);
-                    if (op != 0 && d == 0) {
-                        status = kStInternal | kDetNoStep;
+                    k = min(min(match_run(i, j), rem), min(min(n_w - i, m_w - j), C - i));
+                    if (k > 0) {
                         op = 0;
+                    } else {
+                        k = 1;
+                        const int q = j + off;
+                        const int r = q % L, p = q / L;
+                        const uint32_t xw = xy[((i * 2 + 0) * 32 + lane) * L + r];
+                        const uint32_t yw = xy[((i * 2 + 1) * 32 + lane) * L + r];
+                        op = (xw >> (31 - p)) & 1u ? 1 : ((yw >> (31 - p)) & 1u ? 3 : 2);
+                        if (d == 0) status = kStInternal | kDetNoStep;
                     }
+                    c_reads += static_cast<unsigned long long>(k) * (d == 0 ? 1u : 3u);
                 }
-                i += op != 2;
-                j += op != 3;
-                d -= op != 0;
-                ++steps;
-                if (op != 0) ++dist;
-                emit(op, 1);
+                i += op != 2 ? k : 0;
+                j += op != 3 ? k : 0;
+                if (op != 0) {
+                    d -= k;
+                    dist += k;
+                }
+                steps += k;
+                emit(op, k);
+                write_pending();
             }
             if (cont && status == 0) {
                 // the window continues on the suffix t[i:n_w) x p[j:m_w)
@@ -699,20 +758,14 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
                 d0 = 0;
                 found_d = -1;
                 expect_d = d;
-                load_segment();
+                need_load = true;
             } else {
                 if (!cont && limit < 0 && d != 0) status = kStInternal | kDetLeftover;
                 toff += i;
                 poff += j;
                 ++nwin;
                 if (nwin > window_cap) status = kStInternal | kDetWatchdog;
-                bool more = status == 0 && next_window();
-                while (!more) {
-                    finish_pair();
-                    fetch();
-                    if (pair < 0) break;
-                    more = next_window();
-                }
+                need_window = true;
             }
         }
     }
@@ -829,7 +882,7 @@ int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_blo
 }
 
 size_t bnd_scratch_bytes(int L, long long total_warps) {
-    return static_cast<size_t>(total_warps) * static_cast<size_t>(32 * L + 1) * 32 * L * 4;
+    return static_cast<size_t>(total_warps) * static_cast<size_t>(32 * L + 4) * 32 * L * 4;
 }
 
 int k1_warps_per_block(int L) {

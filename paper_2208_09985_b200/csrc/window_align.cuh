@@ -54,6 +54,7 @@ struct AlignParams {
     const int32_t* order;     // processing order (null = identity)
     int32_t n_pairs;
     int32_t W, O, et, policy; // policy: 0 BaselineEdges, 1 SeneEntries, 2 DentTrimmed (counters)
+    int32_t two;              // the constant 2 at run time (keeps the DP shift an IMAD)
     // outputs
     int32_t* distance;
     int32_t* windows;
