@@ -467,6 +467,8 @@ struct RunConfig {
     int L, W, O, et, policy;
 };
 
+unsigned long long* g_phase_buf = nullptr;  // diagnostics (SG_PHASE_CYCLES=1)
+
 RunConfig run_config(const sg_config* c) {
     RunConfig r;
     r.L = limbs_for(c->W);
@@ -575,6 +577,16 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.scratch = st.scratch.as<uint32_t>();
     p.bnd = st.bnd.as<uint32_t>();
     p.next_pair = st.next_pair.as<unsigned int>();
+    p.phase_cycles = nullptr;
+    if (const char* e = getenv("SG_PHASE_CYCLES")) {
+        if (e[0] == '1') {
+            static unsigned long long* dbuf = nullptr;
+            if (!dbuf) SG_CUDA_CHECK(cudaMalloc(&dbuf, 64));
+            SG_CUDA_CHECK(cudaMemsetAsync(dbuf, 0, 64, st.stream));
+            p.phase_cycles = dbuf;
+            g_phase_buf = dbuf;
+        }
+    }
 
     int launches = 0;
     SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
@@ -1092,6 +1104,15 @@ int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* 
 }
 
 void sg_session_destroy(sg_session* s) { delete s; }
+
+/* Diagnostics: per-phase SM cycles summed over warps of the last run with
+ * SG_PHASE_CYCLES=1 (setup, DC, TB+advance, iterations). Not part of the ABI
+ * header. */
+int sg_debug_phase_cycles(unsigned long long* out4) {
+    if (!g_phase_buf) return -1;
+    cudaMemcpy(out4, g_phase_buf, 32, cudaMemcpyDeviceToHost);
+    return 0;
+}
 
 int64_t sg_last_transfer_bytes(int direction) { return direction ? g_last_d2h : g_last_h2d; }
 

@@ -16,9 +16,10 @@ constexpr unsigned kFull = 0xffffffffu;
 // range, wider windows continue as a new segment), WARPS warps per block
 // (warps are independent; blocks only share an SM).
 template <int L> struct KCfg;
-template <> struct KCfg<1> { static constexpr int R = 8, C = 32, WARPS = 4; };
-template <> struct KCfg<2> { static constexpr int R = 8, C = 40, WARPS = 4; };
+template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4; };
+template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4; };
 template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
+// (R = 4: sweep groups are aligned to 4-column text-code words; C % 4 == 0.)
 
 // Shared memory of one warp, in 32-bit words:
 //   txt [WB/8][32] u64   text codes (1 byte per column, 4 = non-ACGT / virtual)
@@ -26,7 +27,7 @@ template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
 //   pm  [5][32][L]       pattern masks per code (code 4: all ones)
 //   sq  [6L+4][32]       packed text (2L+1 words), pattern (2L+1), text N (L+1),
 //                        pattern N (L+1) of the current segment, for traceback
-template <int L> __host__ __device__ constexpr int txt_words() { return (32 * L / 8) * 32 * 2; }
+template <int L> __host__ __device__ constexpr int txt_words() { return (32 * L / 4 + 2) * 32; }
 template <int L> __host__ __device__ constexpr int xy_words() {
     return (KCfg<L>::C + 1) * 2 * 32 * L;
 }
@@ -188,7 +189,7 @@ struct Sweep {
 };
 
 // One cell of row r. bI / bM: boundary bits (0/1).
-template <int L, int R, int SLOT, bool FIRST>
+template <int L, int R, int SLOT, bool FIRST, bool CAP>
 __device__ __forceinline__ void sweep_cell(Sweep<L, R>& S, int r, const uint32_t (&north)[L],
                                            uint32_t two, uint32_t bI, uint32_t bM) {
     uint32_t east[L], diag[L], I[L], M[L], Sv[L], Rv[L];
@@ -209,7 +210,7 @@ __device__ __forceinline__ void sweep_cell(Sweep<L, R>& S, int r, const uint32_t
 #pragma unroll
     for (int l = 0; l < L; ++l) Rv[l] = I[l] & diag[l] & Sv[l] & (M[l] | S.pmq[SLOT][l]);
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
+    for (int l = 0; l < L && CAP; ++l) {
         const uint32_t x = Rv[l] & ~M[l], y = Rv[l] & ~east[l];
         if (FIRST) {
             S.acc[SLOT][0][l] = x;
@@ -229,68 +230,34 @@ __device__ __forceinline__ void sweep_cell(Sweep<L, R>& S, int r, const uint32_t
 
 // Rows TOP, TOP-1, ..., TOP-|Rs|+1 of step U (descending: a row reads its
 // north neighbour's value from the previous step before that row updates).
-template <int L, int R, int U, int TOP, int... Rs>
+template <int L, int R, int U, int TOP, bool CAP, int... Rs>
 __device__ __forceinline__ void sweep_rows(Sweep<L, R>& S, const uint32_t (&t)[R + 1],
                                            uint32_t two, std::integer_sequence<int, Rs...>) {
-    (sweep_cell<L, R, ((U - (TOP - Rs)) & (R - 1)), false>(S, TOP - Rs, S.v[TOP - Rs - 1], two,
-                                                           t[TOP - Rs], t[TOP - Rs + 1]),
+    (sweep_cell<L, R, ((U - (TOP - Rs)) & (R - 1)), false, CAP>(S, TOP - Rs, S.v[TOP - Rs - 1],
+                                                                two, t[TOP - Rs],
+                                                                t[TOP - Rs + 1]),
      ...);
 }
 
-// Step U (static) of a group. When `slow` (warp-uniform), the boundary bits
-// come from g = n_w - S0 - d0 + s: row r gets [g >= 2r] (or d == 0) and
-// [g >= 2r + 2] (dp.cpp:187-195 with c = n - i: [c > d-1], [c-1 > d]);
-// otherwise every cell is at least two columns from the edge and both are 1.
-template <int L, int R, int U>
+// Step U (static) of a group. SLOW: explicit boundary bits from
+// g = n_w - S0 - d0 + s: row r gets [g >= 2r] (or d == 0) and [g >= 2r + 2]
+// (dp.cpp:187-195 with c = n - i: [c > d-1], [c-1 > d]). Fast groups have
+// every cell at least two columns from the right edge: both bits are 1.
+// CAP: accumulate traceback events.
+template <int L, int R, int U, bool SLOW, bool CAP>
 __device__ __forceinline__ void sweep_step(Sweep<L, R>& S, const uint32_t (&north0)[L],
                                            const uint32_t (&pm0)[L], uint32_t two, uint32_t one,
-                                           int g, bool z0, bool slow) {
+                                           int g, bool z0) {
 #pragma unroll
     for (int l = 0; l < L; ++l) S.pmq[U][l] = pm0[l];
     uint32_t t[R + 1];
-    if (slow) {
 #pragma unroll
-        for (int k = 0; k <= R; ++k) t[k] = static_cast<uint32_t>(g >= 2 * k);
-        t[0] |= static_cast<uint32_t>(z0);
-    } else {
-#pragma unroll
-        for (int k = 0; k <= R; ++k) t[k] = one;
-    }
-    sweep_rows<L, R, U, R - 1>(S, t, two, std::make_integer_sequence<int, R - 1>{});
-    sweep_cell<L, R, U, true>(S, 0, north0, two, t[0], t[1]);
+    for (int k = 0; k <= R; ++k) t[k] = SLOW ? static_cast<uint32_t>(g >= 2 * k) : one;
+    if (SLOW) t[0] |= static_cast<uint32_t>(z0);
+    sweep_rows<L, R, U, R - 1, CAP>(S, t, two, std::make_integer_sequence<int, R - 1>{});
+    sweep_cell<L, R, U, true, CAP>(S, 0, north0, two, t[0], t[1]);
 #pragma unroll
     for (int l = 0; l < L; ++l) S.dg[0][l] = north0[l];
-}
-
-// Side effects of the column row R-1 just finished (static ring SLOT): park
-// its value for the next chunk, store the column's events (OR-ed into the
-// earlier chunks' events). Out-of-range columns go to the dummy slots.
-template <int L, int R, int C, int SLOT>
-__device__ __forceinline__ void finish_col(const Sweep<L, R>& S, int colf, int n_w,
-                                           bool any_parked, uint32_t keep_old,
-                                           uint32_t* __restrict__ xy, uint32_t* __restrict__ bnd,
-                                           int lane) {
-    constexpr int WB = 32 * L;
-    const bool real = colf >= 0 && colf < n_w;
-    const int cb = real ? colf + 2 : WB + 2;
-    const int cx = real && colf < C ? colf : C;
-#pragma unroll
-    for (int l = 0; l < L; ++l) bnd[(cb * 32 + lane) * L + l] = S.v[R - 1][l];
-    uint32_t* px = xy + ((cx * 2 + 0) * 32 + lane) * L;
-    uint32_t* py = xy + ((cx * 2 + 1) * 32 + lane) * L;
-    if (any_parked) {  // warp-uniform: some lane is past its first chunk
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            px[l] = (px[l] & keep_old) | S.acc[SLOT][0][l];
-            py[l] = (py[l] & keep_old) | S.acc[SLOT][1][l];
-        }
-    } else {
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            px[l] = S.acc[SLOT][0][l];
-            py[l] = S.acc[SLOT][1][l];
-        }
-    }
 }
 
 // Bit j = 0 of row r's value at column 0 (the d_opt test, dp.cpp:222).
@@ -302,61 +269,120 @@ __device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0,
     return (v >> (31 - p0)) & 1u;
 }
 
-// Parked-row layout (per lane): slot c + 2 holds column c (slots 0 and 1 pad
-// the two-step-ahead prefetch past column 0), slot WB + 2 is the dummy store
-// target for virtual columns, slot WB + 3 holds R[n][d0 - 1] for first chunks.
-template <int L> __device__ __forceinline__ int bslot(int col) { return col + 2; }
+// Per-lane views of the warp's shared memory and parked-row scratch.
+//   bnd (stride 32L words): slot c + 2 = column c (slots 0 / 1 pad the
+//   two-step-ahead prefetch past column 0), WB + 2 = dummy store target.
+//   xy (stride 64L words per column, +32L for Y): column C is the dummy.
+//   txt: 4 text codes per word, word w + 1 = columns 4w..4w+3 (word 0 pads
+//   column -1 with code 4).
+template <int L>
+struct LaneMem {
+    uint32_t* bnd;        // + lane * L
+    uint32_t* xy;         // + lane * L
+    const uint32_t* pm;   // + lane * L
+    const uint32_t* txt;  // + lane
+};
 
-// One group of R steps (static ring slots). `drain` (warp-uniform) marks the
-// group after row 0 reached column 0: rows 1..R-1 finish their last columns
-// (rows already past column 0 compute harmless values on negative columns)
-// and each row's bit j = 0 at column 0 is tested as it gets there.
-template <int L, int R, int C>
-__device__ __forceinline__ void sweep_group(Sweep<L, R>& S, uint32_t (&nbr)[2][L],
-                                            const uint32_t* __restrict__ nbp, int nstride,
-                                            uint64_t codes8, int col_top,
-                                            const uint32_t* __restrict__ pmv, uint32_t two,
-                                            uint32_t one, int g0, bool z0, bool slow, bool drain,
-                                            int n_w, bool any_parked, uint32_t keep_old,
-                                            uint32_t* __restrict__ xy,
-                                            uint32_t* __restrict__ bnd, int lane, int r0,
-                                            int p0, int& fr) {
+// Prefetch rings carried across steps and groups: the parked row for two
+// steps ahead (nbr), the pattern mask of the next column (pmn) and the earlier
+// chunks' events of the next finished column (ox / oy, raw).
+template <int L>
+struct Pref {
+    uint32_t nbr[2][L];
+    uint32_t pmn[L];
+    uint32_t ox[L], oy[L];
+};
+
+template <int C>
+__device__ __forceinline__ int xslot(int col, int n_w) {
+    return col >= 0 && col < n_w && col < C ? col : C;
+}
+
+enum { kSlow = 0, kIn = 1, kOut = 2 };
+
+// One group of R = 4 steps (static ring slots) covering row-0 columns
+// col_top..col_top-3 (col_top = 3 mod 4). MODE kSlow: near the right edge
+// (explicit boundary bits, virtual columns, dummy slots); kIn: every finished
+// column is a real traceback-code column (static addressing); kOut: every
+// cell lies right of the traceback-code region (no event capture or stores).
+// DRAIN: the extra group after row 0 left column 0 (rows 1..R-1 finish; rows
+// past column 0 compute harmless values on negative columns; each row's
+// bit j = 0 is tested when it reaches column 0).
+template <int L, int R, int C, int MODE, bool DRAIN>
+__device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const LaneMem<L>& M,
+                                            uint32_t codes4, uint32_t codes4n, int col_top,
+                                            uint32_t two, uint32_t one, int g0, bool z0, int n_w,
+                                            uint32_t keep_old, int r0, int p0, int& fr) {
+    static_assert(R == 4, "groups are aligned to 4-column text-code words");
+    constexpr int WB = 32 * L;
+    constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
+    // group bases: row-0 parked-row slot of step 0, finished column of step 0
+    const uint32_t* nbg = M.bnd + (col_top + 2) * 32 * L;
+    const int colf0 = col_top + R - 1;
+    uint32_t* pbg = M.bnd + (colf0 + 2) * 32 * L;
+    uint32_t* pxg = M.xy + colf0 * 64 * L;
+    if (CAP) {  // earlier chunks' events of step 0's finished column
+        const uint32_t* po = M.xy + xslot<C>(colf0, n_w) * 64 * L;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            F.ox[l] = po[l];
+            F.oy[l] = po[32 * L + l];
+        }
+    }
 #define SG_STEP(U)                                                                           \
-    if ((U) < R) {                                                                           \
-        constexpr int UU = (U) < R ? (U) : 0;                                                \
-        const int col0 = col_top - UU;                                                       \
-        int code = static_cast<int>((codes8 >> (8 * (col0 & 7))) & 0xFFu);                   \
-        code = col0 >= 0 && col0 < n_w ? code : 4; /* virtual column: all-ones mask */       \
+    if (!DRAIN || (U) + 1 < R) {                                                             \
+        const int col0 = col_top - (U);                                                      \
         uint32_t pm0[L], north0[L];                                                          \
         _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
-            pm0[l] = pmv[(code * 32 + lane) * L + l];                                        \
-            north0[l] = nbr[UU & 1][l];                                                      \
+            pm0[l] = F.pmn[l];                                                               \
+            north0[l] = F.nbr[(U) & 1][l] | ~keep_old; /* first chunk: R[.][-1] = ones */   \
         }                                                                                    \
-        /* prefetch the parked row for step UU + 2 (two steps of latency hiding) */          \
-        const uint32_t* src = nbp - (UU + 2) * nstride;                                      \
-        _Pragma("unroll") for (int l = 0; l < L; ++l) nbr[UU & 1][l] = src[l];               \
-        if (!drain || UU + 1 < R) {                                                          \
-            sweep_step<L, R, UU>(S, north0, pm0, two, one, g0 + UU, z0, slow);               \
-            finish_col<L, R, C, ((UU + 1) & (R - 1))>(S, col0 + R - 1, n_w, any_parked,     \
-                                                       keep_old, xy, bnd, lane);             \
-            if (drain && fr < 0 && UU + 1 < R && !top_bit<L, R>(S, UU + 1, r0, p0))          \
-                fr = UU + 1;                                                                 \
+        {   /* prefetch: parked row two steps ahead, pattern mask of the next column */     \
+            const uint32_t* src = DRAIN ? M.bnd : nbg - ((U) + 2) * 32 * L;                  \
+            _Pragma("unroll") for (int l = 0; l < L; ++l) F.nbr[(U) & 1][l] = src[l];        \
+            const uint32_t w = (U) == 3 ? codes4n : codes4;                                  \
+            const int code = static_cast<int>((w >> (8 * ((2 - (U)) & 3))) & 0xFFu);         \
+            _Pragma("unroll") for (int l = 0; l < L; ++l) F.pmn[l] = M.pm[code * 32 * L + l]; \
         }                                                                                    \
+        sweep_step<L, R, (U), SLOW, CAP>(S, north0, pm0, two, one, g0 + (U), z0);            \
+        {   /* row R-1 finished column colf: park it, store its events */                   \
+            constexpr int SL = ((U) + 1) & (R - 1);                                          \
+            const int colf = colf0 - (U);                                                    \
+            uint32_t* pb = pbg - (U) * 32 * L;                                               \
+            uint32_t* px = pxg - (U) * 64 * L;                                               \
+            if (SLOW) {                                                                      \
+                pb = M.bnd + (colf >= 0 && colf < n_w ? colf + 2 : WB + 2) * 32 * L;         \
+                px = M.xy + xslot<C>(colf, n_w) * 64 * L;                                    \
+            }                                                                                \
+            _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];             \
+            if (CAP) {                                                                       \
+                _Pragma("unroll") for (int l = 0; l < L; ++l) {                              \
+                    px[l] = (F.ox[l] & keep_old) | S.acc[SL][0][l];                          \
+                    px[32 * L + l] = (F.oy[l] & keep_old) | S.acc[SL][1][l];                 \
+                }                                                                            \
+                if ((U) + 1 < R) { /* next step's column; groups reload at their start */   \
+                    const uint32_t* po = SLOW ? M.xy + xslot<C>(colf - 1, n_w) * 64 * L      \
+                                              : px - 64 * L;                                 \
+                    _Pragma("unroll") for (int l = 0; l < L; ++l) {                          \
+                        F.ox[l] = po[l];                                                     \
+                        F.oy[l] = po[32 * L + l];                                            \
+                    }                                                                        \
+                }                                                                            \
+            }                                                                                \
+        }                                                                                    \
+        if (DRAIN && fr < 0 && !top_bit<L, R>(S, ((U) + 1) & (R - 1), r0, p0)) fr = (U) + 1; \
     }
-    SG_STEP(0) SG_STEP(1) SG_STEP(2) SG_STEP(3) SG_STEP(4) SG_STEP(5) SG_STEP(6) SG_STEP(7)
+    SG_STEP(0) SG_STEP(1) SG_STEP(2) SG_STEP(3)
 #undef SG_STEP
 }
 
 // One chunk of rows d0..d0+R-1 over columns n_w-1..0 (n_w = 0: idle lane).
 // Returns the first row r of the chunk with bit j=0 of R[0][d0+r] clear, or -1.
 template <int L, int R, int C>
-__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, bool any_parked,
-                                        uint32_t two, uint32_t one,
-                                        const uint32_t* __restrict__ pmv,
-                                        const uint64_t* __restrict__ txt, uint32_t* __restrict__ xy,
-                                        uint32_t* __restrict__ bnd, int lane) {
+__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, uint32_t two,
+                                        uint32_t one, const LaneMem<L>& M) {
     constexpr int WB = 32 * L;
-    static_assert((R & (R - 1)) == 0 && R <= 8 && WB % R == 0, "R must be a power of two <= 8");
+    static_assert(R == 4 && WB % R == 0 && C % R == 0, "R = 4 groups aligned to C");
     Sweep<L, R> S;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -375,39 +401,48 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, boo
     const int S0 = tsteps - 1;
     const bool z0 = d0 == 0;
     const uint32_t keep_old = d0 > 0 ? ~0u : 0u;
-    // Row-0 north inputs: the parked row d0-1. First chunks read R[n][-1] from
-    // slot WB+3 (stride 0); virtual columns >= n_w hold R[n][d0-1] (filled here).
-    uint32_t* const init_slot = bnd + ((WB + 3) * 32 + lane) * L;
-#pragma unroll
-    for (int l = 0; l < L; ++l) init_slot[l] = init_limb<L>(d0 - 1, l);
+    // Virtual columns >= n_w of the parked row hold R[n][d0-1].
     if (d0 > 0)
         for (int c = n_w; c <= S0; ++c)
 #pragma unroll
-            for (int l = 0; l < L; ++l)
-                bnd[(bslot<L>(c) * 32 + lane) * L + l] = init_limb<L>(d0 - 1, l);
-    const int nstride = d0 > 0 ? 32 * L : 0;
-    const uint32_t* nbp0 = d0 > 0 ? bnd + (bslot<L>(S0) * 32 + lane) * L : init_slot;
-    uint32_t nbr[2][L];
+            for (int l = 0; l < L; ++l) M.bnd[(c + 2) * 32 * L + l] = init_limb<L>(d0 - 1, l);
+    Pref<L> F;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-        nbr[0][l] = nbp0[l];
-        nbr[1][l] = nbp0[l - nstride];
+        F.nbr[0][l] = M.bnd[(S0 + 2) * 32 * L + l];
+        F.nbr[1][l] = M.bnd[(S0 + 1) * 32 * L + l];
+    }
+    uint32_t codes4 = M.txt[((S0 >> 2) + 1) * 32];
+    {
+        const int code = static_cast<int>((codes4 >> 24) & 0xFFu);  // column S0 = 3 mod 4
+#pragma unroll
+        for (int l = 0; l < L; ++l) F.pmn[l] = M.pm[code * 32 * L + l];
     }
     const int off = WB - m_w;
     const int r0 = off % L, p0 = off / L;
     int fr = -1;
-    for (int sg = 0; sg <= tsteps; sg += R) {
-        const bool drain = sg == tsteps;  // the extra group: rows 1..R-1 finish
+    for (int sg = 0; sg < tsteps; sg += R) {
         const int col_top = S0 - sg;
-        const uint32_t* nbp = drain ? init_slot : nbp0 - sg * nstride;
-        const uint64_t codes8 = txt[((col_top < 0 ? 0 : col_top) >> 3) * 32 + lane];
+        const uint32_t codes4n = M.txt[(col_top >> 2) * 32];  // word of column col_top - 4
         const int g0 = n_w - S0 - d0 + sg;
-        const bool slow = drain || __any_sync(kFull, n_w > 0 && g0 < 2 * R);
-        if (drain && !top_bit<L, R>(S, 0, r0, p0)) fr = 0;  // row 0 just left column 0
-        sweep_group<L, R, C>(S, nbr, nbp, drain ? 0 : nstride, codes8, col_top, pmv, two, one,
-                             g0, z0, slow, drain, n_w, any_parked, keep_old, xy, bnd, lane, r0,
-                             p0, fr);
+        if (__any_sync(kFull, n_w > 0 && g0 < 2 * R))
+            sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
+                                               z0, n_w, keep_old, r0, p0, fr);
+        else if (col_top - R + 1 >= C)
+            sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
+                                              z0, n_w, keep_old, r0, p0, fr);
+        else if (col_top + R - 1 < C)
+            sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
+                                             n_w, keep_old, r0, p0, fr);
+        else
+            sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
+                                               z0, n_w, keep_old, r0, p0, fr);
+        codes4 = codes4n;
     }
+    // drain: rows 1..R-1 finish (row 0 has just left column 0)
+    if (!top_bit<L, R>(S, 0, r0, p0)) fr = 0;
+    sweep_group<L, R, C, kSlow, true>(S, F, M, codes4, codes4, -1, two, one,
+                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, r0, p0, fr);
     return fr;
 }
 
@@ -432,11 +467,14 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
     uint32_t* const bnd = P.bnd + gwarp * (WB + 4) * 32 * L;    // [WB+4][32][L]
     const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
+    const LaneMem<L> lmem{bnd + lane * L, xy + lane * L, pmv + lane * L,
+                          reinterpret_cast<const uint32_t*>(txt) + lane};
 
 #pragma unroll
     for (int l = 0; l < L; ++l) pmv[(4 * 32 + lane) * L + l] = ~0u;  // non-ACGT text
 #pragma unroll
-    for (int b = 0; b < WB / 8; ++b) txt[b * 32 + lane] = 0x0404040404040404ull;  // idle lanes
+    for (int b = 0; b <= WB / 4; ++b)  // idle lanes and the column -1 pad: code 4
+        reinterpret_cast<uint32_t*>(txt)[b * 32 + lane] = 0x04040404u;
 
     const int W = P.W;
     const int step_limit = W - P.O;
@@ -525,13 +563,17 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         // are mapped to code 4 by the sweep itself
         uint32_t* const txt32 = reinterpret_cast<uint32_t*>(txt);
 #pragma unroll
-        for (int h = 0; h < WB / 4; ++h) {  // 4 columns per 32-bit half
+        for (int h = 0; h < WB / 4; ++h) {  // word h + 1: columns 4h..4h+3
             uint32_t c = spread4(tw[h >> 2] >> (8 * (h & 3)));
             if (hasn) {
                 const uint32_t nm = spread4bits(tn[h >> 3] >> (4 * (h & 7))) * 0xFFu;
                 c = (c & ~nm) | (0x04040404u & nm);
             }
-            txt32[((h >> 1) * 32 + lane) * 2 + (h & 1)] = c;
+            // columns >= n_w are virtual: code 4 (all-ones mask)
+            const int valid = n_w - 4 * h;
+            if (valid < 4) c = valid <= 0 ? 0x04040404u : (c & (0xFFFFFFFFu >> (8 * (4 - valid))))
+                                                          | (0x04040404u << (8 * valid));
+            txt32[(h + 1) * 32 + lane] = c;
         }
         // packed sequences for the traceback's match runs
 #pragma unroll
@@ -641,7 +683,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     };
 
     bool need_pair = true, need_window = false, need_load = false;
+    unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0;
     for (;;) {
+        const long long ck0 = clock64();
         // ---------------------------------------------- per-lane setup
         while (need_pair || need_window) {
             if (need_pair) {
@@ -665,12 +709,17 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         }
         const bool in_dc = pair >= 0;
         if (!__any_sync(kFull, in_dc)) break;
+        __syncwarp();
+        const long long ck1 = clock64();
 
         // ------------------------------------------------ DC: one chunk
         const int n_max = warp_max(in_dc ? n_w : 0);
-        const bool any_parked = __any_sync(kFull, in_dc && d0 > 0);
-        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, any_parked, two, one,
-                                         pmv, txt, xy, bnd, lane);
+        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, two, one, lmem);
+        __syncwarp();
+        const long long ck2 = clock64();
+        ph_setup += ck1 - ck0;
+        ph_dc += ck2 - ck1;
+        ++ph_it;
 
         // ------------------------------------------------ d_opt detection
         bool solved = false;
@@ -768,6 +817,14 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
                 need_window = true;
             }
         }
+        __syncwarp();
+        ph_tb += clock64() - ck2;
+    }
+    if (P.phase_cycles && lane == 0) {
+        atomicAdd(P.phase_cycles + 0, ph_setup);
+        atomicAdd(P.phase_cycles + 1, ph_dc);
+        atomicAdd(P.phase_cycles + 2, ph_tb);
+        atomicAdd(P.phase_cycles + 3, ph_it);
     }
 }
 

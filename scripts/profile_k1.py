@@ -18,3 +18,10 @@ for _ in range(a.runs):
     print(f"cfg{a.cfg} pairs={a.pairs} K1-K3 {ms:.3f} ms  K1 {k1:.3f} ms  {a.pairs / (ms / 1e3):.0f} aln/s  {s.info()}", flush=True)
 r = s.fetch()
 print("cells_computed", r.total.cells_computed, "ALG_OPS/s (K1)", 4 * ((a.W + 31) // 32) * r.total.cells_computed / (k1 / 1e3) / 1e12, "T")
+if os.environ.get("SG_PHASE_CYCLES") == "1":
+    import ctypes as C
+    from paper_2208_09985_b200 import _ffi
+    buf = (C.c_ulonglong * 4)()
+    _ffi.load().sg_debug_phase_cycles(buf)
+    tot = buf[0] + buf[1] + buf[2]
+    print(f"phase cycles (sum over warps): setup {buf[0]/tot:.1%}  DC {buf[1]/tot:.1%}  TB {buf[2]/tot:.1%}  iterations {buf[3]}  cycles/iter {tot/max(buf[3],1):.0f}")
