@@ -263,8 +263,10 @@ def main_ours(args):
     pairs = args.pairs
     cfg = sg.AlignerConfig(W=W, O=O, sene=True, dent=True, early_termination=True)
 
+    from paper_2208_09985_b200 import shard
+    first, count = shard.rank_range(rank, ws, pairs)
     t_gen = time.perf_counter()
-    batch = sg.synth_packed(CFG_ID, rank * pairs, pairs)
+    batch = sg.synth_packed(CFG_ID, first, count)
     t_gen = time.perf_counter() - t_gen
     sess = sg.Session(cfg, batch, device)
 

@@ -206,14 +206,18 @@ struct DevSlot {
     std::mutex mu;
     std::unique_ptr<DevState> st;
 };
+// Keyed by (device, occurrence): a device listed twice in one call gets two
+// pipelines (own buffers), so shards never share or wait on each other.
 // Intentionally leaked: no device teardown races the CUDA runtime at exit.
 std::mutex g_slots_mu;
-std::vector<DevSlot*>* g_slots = new std::vector<DevSlot*>();
+std::vector<std::vector<DevSlot*>>* g_slots = new std::vector<std::vector<DevSlot*>>();
 
-DevSlot& dev_slot(int dev) {
+DevSlot& dev_slot(int dev, int occurrence) {
     std::lock_guard<std::mutex> lk(g_slots_mu);
-    while (static_cast<int>(g_slots->size()) <= dev) g_slots->push_back(new DevSlot());
-    return *(*g_slots)[static_cast<size_t>(dev)];
+    while (static_cast<int>(g_slots->size()) <= dev) g_slots->emplace_back();
+    auto& v = (*g_slots)[static_cast<size_t>(dev)];
+    while (static_cast<int>(v.size()) <= occurrence) v.push_back(new DevSlot());
+    return *v[static_cast<size_t>(occurrence)];
 }
 
 // ------------------------------------------------------------ validation
@@ -757,7 +761,9 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
         ShardOut& o = so[d];
         try {
             SG_CUDA_CHECK(cudaSetDevice(devices[d]));
-            DevSlot& slot = dev_slot(devices[d]);
+            int occ = 0;
+            for (size_t e = 0; e < d; ++e) occ += devices[e] == devices[d];
+            DevSlot& slot = dev_slot(devices[d], occ);
             locks[d] = std::unique_lock<std::mutex>(slot.mu);
             if (!slot.st) {
                 slot.st = std::make_unique<DevState>();
