@@ -488,9 +488,9 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp) {
     const sg_packed_pairs* in = s.in;
     const int64_t words = pp.word_hi - pp.word_lo;
     int64_t h2d_bytes = 0;
-    const size_t seq_bytes = 4 * static_cast<size_t>(words + 8);
+    const size_t seq_bytes = 4 * static_cast<size_t>(words + 24);  // K1 reads up to 12 words past a start
     st.seq.ensure(seq_bytes);
-    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 8, in->seq_words - pp.word_lo));
+    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 24, in->seq_words - pp.word_lo));
     if (avail > 0) {
         SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.p, in->seq + pp.word_lo, 4 * static_cast<size_t>(avail),
                                       cudaMemcpyHostToDevice, st.stream));

@@ -32,7 +32,12 @@ template <int L> __host__ __device__ constexpr int xy_words() {
     return (KCfg<L>::C + 1) * 2 * 32 * L;
 }
 template <int L> __host__ __device__ constexpr int pm_words() { return 5 * L * 32; }
-template <int L> __host__ __device__ constexpr int sq_words() { return (6 * L + 4) * 32; }
+// words of packed text / pattern staged per lane: the window plus the reach
+// of the next window's start (W - O <= 64 for L <= 2)
+template <int L> __host__ __device__ constexpr int pf_words() { return L == 1 ? 6 : L == 2 ? 10 : 12; }
+template <int L> __host__ __device__ constexpr int sq_words() {
+    return (2 * pf_words<L>() + 2 * (L + 1)) * 32;
+}
 template <int L> __host__ __device__ constexpr int warp_smem_words() {
     return txt_words<L>() + xy_words<L>() + pm_words<L>() + sq_words<L>();
 }
@@ -270,8 +275,8 @@ __device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0,
 }
 
 // Per-lane views of the warp's shared memory and parked-row scratch.
-//   bnd (stride 32L words): slot c + 2 = column c (slots 0 / 1 pad the
-//   two-step-ahead prefetch past column 0), WB + 2 = dummy store target.
+//   bnd (stride 32L words): slot c + 4 = column c (slots 0..3 pad the
+//   one-group-ahead prefetch past column 0), WB + 4 = dummy store target.
 //   xy (stride 64L words per column, +32L for Y): column C is the dummy.
 //   txt: 4 text codes per word, word w + 1 = columns 4w..4w+3 (word 0 pads
 //   column -1 with code 4).
@@ -288,7 +293,7 @@ struct LaneMem {
 // chunks' events of the next finished column (ox / oy, raw).
 template <int L>
 struct Pref {
-    uint32_t nbr[2][L];
+    uint32_t nbr[4][L];
     uint32_t pmn[L];
     uint32_t ox[L], oy[L];
 };
@@ -317,9 +322,9 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
     constexpr int WB = 32 * L;
     constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
     // group bases: row-0 parked-row slot of step 0, finished column of step 0
-    const uint32_t* nbg = M.bnd + (col_top + 2) * 32 * L;
+    const uint32_t* nbg = M.bnd + (col_top + 4) * 32 * L;
     const int colf0 = col_top + R - 1;
-    uint32_t* pbg = M.bnd + (colf0 + 2) * 32 * L;
+    uint32_t* pbg = M.bnd + (colf0 + 4) * 32 * L;
     uint32_t* pxg = M.xy + colf0 * 64 * L;
     if (CAP) {  // earlier chunks' events of step 0's finished column
         const uint32_t* po = M.xy + xslot<C>(colf0, n_w) * 64 * L;
@@ -335,11 +340,11 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
         uint32_t pm0[L], north0[L];                                                          \
         _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
             pm0[l] = F.pmn[l];                                                               \
-            north0[l] = F.nbr[(U) & 1][l] | ~keep_old; /* first chunk: R[.][-1] = ones */   \
+            north0[l] = F.nbr[(U)][l] | ~keep_old; /* first chunk: R[.][-1] = ones */       \
         }                                                                                    \
-        {   /* prefetch: parked row two steps ahead, pattern mask of the next column */     \
-            const uint32_t* src = DRAIN ? M.bnd : nbg - ((U) + 2) * 32 * L;                  \
-            _Pragma("unroll") for (int l = 0; l < L; ++l) F.nbr[(U) & 1][l] = src[l];        \
+        {   /* prefetch: parked row one group ahead, pattern mask of the next column */     \
+            const uint32_t* src = DRAIN ? M.bnd : nbg - ((U) + 4) * 32 * L;                  \
+            _Pragma("unroll") for (int l = 0; l < L; ++l) F.nbr[(U)][l] = src[l];            \
             const uint32_t w = (U) == 3 ? codes4n : codes4;                                  \
             const int code = static_cast<int>((w >> (8 * ((2 - (U)) & 3))) & 0xFFu);         \
             _Pragma("unroll") for (int l = 0; l < L; ++l) F.pmn[l] = M.pm[code * 32 * L + l]; \
@@ -351,7 +356,7 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
             uint32_t* pb = pbg - (U) * 32 * L;                                               \
             uint32_t* px = pxg - (U) * 64 * L;                                               \
             if (SLOW) {                                                                      \
-                pb = M.bnd + (colf >= 0 && colf < n_w ? colf + 2 : WB + 2) * 32 * L;         \
+                pb = M.bnd + (colf >= 0 && colf < n_w ? colf + 4 : WB + 4) * 32 * L;         \
                 px = M.xy + xslot<C>(colf, n_w) * 64 * L;                                    \
             }                                                                                \
             _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];             \
@@ -405,13 +410,12 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, uin
     if (d0 > 0)
         for (int c = n_w; c <= S0; ++c)
 #pragma unroll
-            for (int l = 0; l < L; ++l) M.bnd[(c + 2) * 32 * L + l] = init_limb<L>(d0 - 1, l);
+            for (int l = 0; l < L; ++l) M.bnd[(c + 4) * 32 * L + l] = init_limb<L>(d0 - 1, l);
     Pref<L> F;
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        F.nbr[0][l] = M.bnd[(S0 + 2) * 32 * L + l];
-        F.nbr[1][l] = M.bnd[(S0 + 1) * 32 * L + l];
-    }
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int l = 0; l < L; ++l) F.nbr[u][l] = M.bnd[(S0 - u + 4) * 32 * L + l];
     uint32_t codes4 = M.txt[((S0 >> 2) + 1) * 32];
     {
         const int code = static_cast<int>((codes4 >> 24) & 0xFFu);  // column S0 = 3 mod 4
@@ -425,15 +429,17 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, uin
         const int col_top = S0 - sg;
         const uint32_t codes4n = M.txt[(col_top >> 2) * 32];  // word of column col_top - 4
         const int g0 = n_w - S0 - d0 + sg;
-        if (__any_sync(kFull, n_w > 0 && g0 < 2 * R))
-            sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                               z0, n_w, keep_old, r0, p0, fr);
-        else if (col_top - R + 1 >= C)
-            sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                              z0, n_w, keep_old, r0, p0, fr);
-        else if (col_top + R - 1 < C)
+        int mode = kSlow;  // warp-uniform
+        if (!__any_sync(kFull, n_w > 0 && g0 < 2 * R)) {
+            if (col_top - R + 1 >= C) mode = kOut;
+            else if (col_top + R - 1 < C) mode = kIn;
+        }
+        if (mode == kIn)
             sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
                                              n_w, keep_old, r0, p0, fr);
+        else if (mode == kOut)
+            sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
+                                              z0, n_w, keep_old, r0, p0, fr);
         else
             sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
                                                z0, n_w, keep_old, r0, p0, fr);
@@ -460,12 +466,13 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     uint32_t* const xy = wbase + txt_words<L>();                 // [C+1][2][32][L]
     uint32_t* const pmv = xy + xy_words<L>();                    // [5][32][L]
     uint32_t* const sq = pmv + pm_words<L>();                    // [6L+4][32]
-    uint32_t* const sq_t = sq;                                   // text words   (NW+1)
-    uint32_t* const sq_p = sq + (NW + 1) * 32;                   // pattern words (NW+1)
-    uint32_t* const sq_tn = sq + (2 * NW + 2) * 32;              // text N words (L+1)
-    uint32_t* const sq_pn = sq + (2 * NW + 3 + L) * 32;          // pattern N words (L+1)
+    constexpr int PFW = pf_words<L>();
+    uint32_t* const sq_t = sq;                                   // text staging (PFW words)
+    uint32_t* const sq_p = sq + PFW * 32;                        // pattern staging (PFW)
+    uint32_t* const sq_tn = sq + 2 * PFW * 32;                   // text N words (L+1)
+    uint32_t* const sq_pn = sq + (2 * PFW + L + 1) * 32;         // pattern N words (L+1)
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
-    uint32_t* const bnd = P.bnd + gwarp * (WB + 4) * 32 * L;    // [WB+4][32][L]
+    uint32_t* const bnd = P.bnd + gwarp * (WB + 5) * 32 * L;    // [WB+5][32][L]
     const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
     const LaneMem<L> lmem{bnd + lane * L, xy + lane * L, pmv + lane * L,
                           reinterpret_cast<const uint32_t*>(txt) + lane};
@@ -489,6 +496,13 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     int d0 = 0, found_d = -1, expect_d = -1;
     int dist = 0, nwin = 0, status = 0;
     int window_cap = 0;
+    // Sequence staging: sq_t / sq_p hold PFW packed words from word st_tw / st_pw;
+    // the segment's text / pattern start at base t_sh / p_sh inside them. The
+    // words of the region the next window can start in are prefetched into
+    // registers (nx_t / nx_p) while the current window runs.
+    uint32_t nx_t[PFW], nx_p[PFW];
+    int64_t nx_tw = -1, nx_pw = -1;
+    int t_sh = 0, p_sh = 0;
     // output
     uint32_t* outw = nullptr;
     int out_bytes = 0, cur_op = -1, acc_n = 0;
@@ -534,8 +548,46 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     auto load_segment = [&]() {
         const int off = WB - m_w;
         uint32_t pw[NW + 1], pn[L + 1], tw[NW + 1], tn[L + 1];
-        load_codes<NW + 1>(P.seq, pbase + poff, pw);
-        load_codes<NW + 1>(P.seq, tbase + toff, tw);
+        {
+            const int64_t ta = tbase + toff, pa = pbase + poff;
+            const int64_t wt = ta >> 4, wp = pa >> 4;
+            // prefetched region usable? (it covers [16 nx_w, 16 (nx_w + PFW)))
+            const bool hit_t = nx_tw >= 0 && wt >= nx_tw && wt + NW + 1 < nx_tw + PFW;
+            const bool hit_p = nx_pw >= 0 && wp >= nx_pw && wp + NW + 1 < nx_pw + PFW;
+            if (!hit_t) {
+                nx_tw = wt;
+#pragma unroll
+                for (int k = 0; k < PFW; ++k) nx_t[k] = __ldg(P.seq + wt + k);
+            }
+            if (!hit_p) {
+                nx_pw = wp;
+#pragma unroll
+                for (int k = 0; k < PFW; ++k) nx_p[k] = __ldg(P.seq + wp + k);
+            }
+#pragma unroll
+            for (int k = 0; k < PFW; ++k) {
+                sq_t[k * 32 + lane] = nx_t[k];
+                sq_p[k * 32 + lane] = nx_p[k];
+            }
+            t_sh = static_cast<int>(ta - 16 * nx_tw);
+            p_sh = static_cast<int>(pa - 16 * nx_pw);
+#pragma unroll
+            for (int k = 0; k <= NW; ++k) {
+                const int bt = t_sh + 16 * k, bp = p_sh + 16 * k;
+                tw[k] = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
+                                        sq_t[((bt >> 4) + 1) * 32 + lane], 2 * (bt & 15));
+                pw[k] = __funnelshift_r(sq_p[(bp >> 4) * 32 + lane],
+                                        sq_p[((bp >> 4) + 1) * 32 + lane], 2 * (bp & 15));
+            }
+            // prefetch the region of the next window (starts <= W - O further on)
+            nx_tw = wt;
+            nx_pw = wp;
+#pragma unroll
+            for (int k = 0; k < PFW; ++k) {
+                nx_t[k] = __ldg(P.seq + wt + k);
+                nx_p[k] = __ldg(P.seq + wp + k);
+            }
+        }
 #pragma unroll
         for (int l = 0; l <= L; ++l) pn[l] = tn[l] = 0;
         if (hasn) {
@@ -575,12 +627,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
                                                           | (0x04040404u << (8 * valid));
             txt32[(h + 1) * 32 + lane] = c;
         }
-        // packed sequences for the traceback's match runs
-#pragma unroll
-        for (int k = 0; k <= NW; ++k) {
-            sq_t[k * 32 + lane] = tw[k];
-            sq_p[k * 32 + lane] = pw[k];
-        }
+        // N words of the segment for the traceback's match runs
 #pragma unroll
         for (int k = 0; k <= L; ++k) {
             sq_tn[k * 32 + lane] = tn[k];
@@ -651,6 +698,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         toff = poff = 0;
         dist = nwin = status = 0;
         window_cap = 4 * ((n_tot + m_tot) / step_limit + 2);  // aligner.cpp:40
+        nx_tw = nx_pw = -1;
         outw = P.scratch + (P.bound_off[pair] >> 2);
         out_bytes = 0;
         cur_op = pend_op = -1;
@@ -662,7 +710,8 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
 
     // Matching bases from (i, j) on (0..16; 0 at a mismatch or a non-ACGT base).
     auto match_run = [&](int i, int j) -> int {
-        const int wi = i >> 4, si = 2 * (i & 15), wj = j >> 4, sj = 2 * (j & 15);
+        const int bi = t_sh + i, bj = p_sh + j;
+        const int wi = bi >> 4, si = 2 * (bi & 15), wj = bj >> 4, sj = 2 * (bj & 15);
         const uint32_t t = __funnelshift_r(sq_t[wi * 32 + lane], sq_t[(wi + 1) * 32 + lane], si);
         const uint32_t p = __funnelshift_r(sq_p[wj * 32 + lane], sq_p[(wj + 1) * 32 + lane], sj);
         uint32_t x = t ^ p;
@@ -772,19 +821,20 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
                     cont = true;
                     break;
                 } else {
+                    // the event words of (i, j) load together with the match-run words
+                    const int q = j + off;
+                    const int r = q % L, p = q / L;
+                    const uint32_t xw = xy[((i * 2 + 0) * 32 + lane) * L + r];
+                    const uint32_t yw = xy[((i * 2 + 1) * 32 + lane) * L + r];
                     k = min(min(match_run(i, j), rem), min(min(n_w - i, m_w - j), C - i));
                     if (k > 0) {
                         op = 0;
                     } else {
                         k = 1;
-                        const int q = j + off;
-                        const int r = q % L, p = q / L;
-                        const uint32_t xw = xy[((i * 2 + 0) * 32 + lane) * L + r];
-                        const uint32_t yw = xy[((i * 2 + 1) * 32 + lane) * L + r];
                         op = (xw >> (31 - p)) & 1u ? 1 : ((yw >> (31 - p)) & 1u ? 3 : 2);
                         if (d == 0) status = kStInternal | kDetNoStep;
                     }
-                    c_reads += static_cast<unsigned long long>(k) * (d == 0 ? 1u : 3u);
+                    c_reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
                 }
                 i += op != 2 ? k : 0;
                 j += op != 3 ? k : 0;
@@ -939,7 +989,7 @@ int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_blo
 }
 
 size_t bnd_scratch_bytes(int L, long long total_warps) {
-    return static_cast<size_t>(total_warps) * static_cast<size_t>(32 * L + 4) * 32 * L * 4;
+    return static_cast<size_t>(total_warps) * static_cast<size_t>(32 * L + 5) * 32 * L * 4;
 }
 
 int k1_warps_per_block(int L) {
