@@ -1112,11 +1112,12 @@ int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* 
 void sg_session_destroy(sg_session* s) { delete s; }
 
 /* Diagnostics: per-phase SM cycles summed over warps of the last run with
- * SG_PHASE_CYCLES=1 (setup, DC, TB+advance, iterations). Not part of the ABI
+ * SG_PHASE_CYCLES=1 (setup, DC, TB+advance, iterations, lanes in DC, TB loop
+ * trips, TB lane-steps, TB entries). Not part of the ABI
  * header. */
-int sg_debug_phase_cycles(unsigned long long* out4) {
+int sg_debug_phase_cycles(unsigned long long* out8) {
     if (!g_phase_buf) return -1;
-    cudaMemcpy(out4, g_phase_buf, 32, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out8, g_phase_buf, 64, cudaMemcpyDeviceToHost);
     return 0;
 }
 

@@ -78,6 +78,16 @@ __device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
     return (b | (b << 7) | (b << 14) | (b << 21)) & 0x01010101u;
 }
 
+// Shared-memory load kept in program order (issued before the arithmetic
+// that follows it in the source).
+__device__ __forceinline__ uint32_t lds_v(const uint32_t* p) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+    return v;
+}
+
 // x*two + b with `two` a runtime 2: an IMAD on the FMA pipe. With a literal 2
 // ptxas emits LEA, which issues on the ALU pipe the bitvector logic needs.
 __device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t two, uint32_t b) {
@@ -505,43 +515,41 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     int t_sh = 0, p_sh = 0;
     // output
     uint32_t* outw = nullptr;
-    int out_bytes = 0, cur_op = -1, acc_n = 0;
-    long long cur_len = 0;
+    int out_bytes = 0, cur_op = -1, cur_len = 0, acc_n = 0;
     uint32_t acc = 0;
     // counters (InstrumentationCounters, proj/include/scrooge/dp.hpp:46-66)
     unsigned long long c_stored = 0, c_writes = 0, c_reads = 0, c_rows = 0, c_cells = 0,
                        c_bequiv = 0;
 
-    // CIGAR runs (cigar_append, proj/src/cigar.cpp:9-16): the open run is
-    // (cur_op, cur_len); a run closed by an op change waits in (pend_op,
-    // pend_len) until the single writer below emits it as bytes
-    // (op << 6) | (len - 1), len 1..64 per byte.
-    int pend_op = -1;
-    long long pend_len = 0;
-    auto emit = [&](int op, long long len) {
-        if (op == cur_op) {
-            cur_len += len;
-        } else {
-            pend_op = cur_op;
-            pend_len = cur_len;
-            cur_op = op;
-            cur_len = len;
+    // CIGAR runs (cigar_append, proj/src/cigar.cpp:9-16) as bytes
+    // (op << 6) | (len - 1): the open byte is (cur_op, cur_len <= 64); it is
+    // written when the op changes or it is full, so a run of length n becomes
+    // ceil(n / 64) bytes (consecutive same-op bytes continue one run).
+    auto put_byte = [&](uint32_t b) {
+        acc |= b << (8 * acc_n);
+        ++out_bytes;
+        if (++acc_n == 4) {
+            *outw++ = acc;
+            acc = 0;
+            acc_n = 0;
         }
     };
-    auto write_pending = [&]() {
-        while (pend_op >= 0) {
-            const long long piece = pend_len > 64 ? 64 : pend_len;
-            acc |= ((static_cast<uint32_t>(pend_op) << 6) | static_cast<uint32_t>(piece - 1))
-                   << (8 * acc_n);
-            ++out_bytes;
-            if (++acc_n == 4) {
-                *outw++ = acc;
-                acc = 0;
-                acc_n = 0;
-            }
-            pend_len -= piece;
-            if (pend_len == 0) pend_op = -1;
+    auto emit = [&](int op, int len) {  // len >= 1
+        if (op == cur_op && cur_len + len <= 64) {
+            cur_len += len;
+            return;
         }
+        if (op == cur_op) {
+            len -= 64 - cur_len;
+            cur_len = 64;
+        }
+        if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
+        while (len > 64) {
+            put_byte((static_cast<uint32_t>(op) << 6) | 63u);
+            len -= 64;
+        }
+        cur_op = op;
+        cur_len = len;
     };
 
     // Pattern masks, text codes and packed sequences of the current segment.
@@ -659,10 +667,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     };
 
     auto finish_pair = [&]() {
-        write_pending();
-        pend_op = cur_op;
-        pend_len = cur_len;
-        write_pending();
+        if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
         if (acc_n) *outw = acc;
         P.distance[pair] = dist;
         P.windows[pair] = nwin;
@@ -701,8 +706,8 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         nx_tw = nx_pw = -1;
         outw = P.scratch + (P.bound_off[pair] >> 2);
         out_bytes = 0;
-        cur_op = pend_op = -1;
-        cur_len = pend_len = 0;
+        cur_op = -1;
+        cur_len = 0;
         acc = 0;
         acc_n = 0;
         c_stored = c_writes = c_reads = c_rows = c_cells = c_bequiv = 0;
@@ -712,9 +717,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     auto match_run = [&](int i, int j) -> int {
         const int bi = t_sh + i, bj = p_sh + j;
         const int wi = bi >> 4, si = 2 * (bi & 15), wj = bj >> 4, sj = 2 * (bj & 15);
-        const uint32_t t = __funnelshift_r(sq_t[wi * 32 + lane], sq_t[(wi + 1) * 32 + lane], si);
-        const uint32_t p = __funnelshift_r(sq_p[wj * 32 + lane], sq_p[(wj + 1) * 32 + lane], sj);
-        uint32_t x = t ^ p;
+        const uint32_t t0 = lds_v(sq_t + wi * 32 + lane), t1 = lds_v(sq_t + (wi + 1) * 32 + lane);
+        const uint32_t p0 = lds_v(sq_p + wj * 32 + lane), p1 = lds_v(sq_p + (wj + 1) * 32 + lane);
+        uint32_t x = __funnelshift_r(t0, t1, si) ^ __funnelshift_r(p0, p1, sj);
         x = (x | (x >> 1)) & 0x55555555u;  // bit 2k: base k differs
         if (hasn) {
             const uint32_t tn = __funnelshift_r(sq_tn[(i >> 5) * 32 + lane],
@@ -728,11 +733,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
             s = (s | (s << 1)) & 0x55555555u;
             x |= s;
         }
-        return x ? (__ffs(x) - 1) >> 1 : 16;
+        return __clz(__brev(x)) >> 1;  // 16 when all 16 bases match
     };
 
     bool need_pair = true, need_window = false, need_load = false;
-    unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0;
+    unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0, ph_act = 0, ph_trips = 0,
+                       ph_steps = 0, ph_tbn = 0;
     for (;;) {
         const long long ck0 = clock64();
         // ---------------------------------------------- per-lane setup
@@ -769,6 +775,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         ph_setup += ck1 - ck0;
         ph_dc += ck2 - ck1;
         ++ph_it;
+        ph_act += __popc(__ballot_sync(kFull, in_dc));
 
         // ------------------------------------------------ d_opt detection
         bool solved = false;
@@ -780,6 +787,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         }
 
         // ------------------------------------------------ TB + advance
+        int tb_trip = 0;
         if (in_dc && solved) {
             if (found_d < 0) status = kStInternal | kDetNoStep;  // aligner.cpp:69-70
             if (first_seg) {
@@ -807,45 +815,66 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
             const int off = WB - m_w;
             int i = 0, j = 0, d = found_d < 0 ? 0 : found_d, steps = 0;
             const int lim = limit >= 0 ? limit : 0x3FFFFFFF;
-            bool cont = false;
+            unsigned reads = 0;
+            ++ph_tbn;
+            // interior: both sides left, inside the stored event columns
             for (;;) {
+                ++ph_steps;
+                ++tb_trip;
                 const int rem = lim - steps;
-                if (rem == 0 || (i == n_w && j == m_w)) break;
-                int op, k;
-                if (i == n_w || j == m_w) {  // one side consumed: the budget is indels
-                    op = i == n_w ? 2 : 3;
-                    const int left = i == n_w ? m_w - j : n_w - i;
-                    if (d != left) status = kStInternal | (i == n_w ? kDetBudgetI : kDetBudgetD);
-                    k = min(rem, left);
-                } else if (i >= C) {
-                    cont = true;
-                    break;
-                } else {
-                    // the event words of (i, j) load together with the match-run words
-                    const int q = j + off;
-                    const int r = q % L, p = q / L;
-                    const uint32_t xw = xy[((i * 2 + 0) * 32 + lane) * L + r];
-                    const uint32_t yw = xy[((i * 2 + 1) * 32 + lane) * L + r];
-                    k = min(min(match_run(i, j), rem), min(min(n_w - i, m_w - j), C - i));
-                    if (k > 0) {
-                        op = 0;
-                    } else {
-                        k = 1;
-                        op = (xw >> (31 - p)) & 1u ? 1 : ((yw >> (31 - p)) & 1u ? 3 : 2);
-                        if (d == 0) status = kStInternal | kDetNoStep;
-                    }
-                    c_reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
-                }
+                if (rem == 0 || i == n_w || j == m_w || i >= C) break;
+                // event words of (i, j) and the match-run words load together
+                const unsigned q = static_cast<unsigned>(j + off);
+                const uint32_t* ev = xy + (i * 64 + lane) * L + q % L;
+                const uint32_t xw = ev[0], yw = ev[32 * L];
+                const uint32_t bit = 0x80000000u >> (q / L);
+                const int run = match_run(i, j);
+                const bool ed = run == 0;  // the other bounds are >= 1 here
+                const int k = ed ? 1 : min(min(run, rem), min(min(n_w - i, m_w - j), C - i));
+                const int op = ed ? (xw & bit ? 1 : (yw & bit ? 3 : 2)) : 0;
+                if (ed && d == 0) status = kStInternal | kDetNoStep;
+                reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
                 i += op != 2 ? k : 0;
                 j += op != 3 ? k : 0;
-                if (op != 0) {
-                    d -= k;
-                    dist += k;
-                }
+                d -= ed;
+                dist += ed;
                 steps += k;
-                emit(op, k);
-                write_pending();
+                // emit (k <= 16): extend the open byte, or write it and open the next
+                if (op == cur_op && cur_len + k <= 64) {
+                    cur_len += k;
+                } else {
+                    const bool same = op == cur_op;
+                    const uint32_t byte = (static_cast<uint32_t>(cur_op) << 6) |
+                                          static_cast<uint32_t>(same ? 63 : cur_len - 1);
+                    if (cur_op >= 0) put_byte(byte);
+                    cur_len = same ? cur_len + k - 64 : k;
+                    cur_op = op;
+                }
             }
+            // tail: one side consumed (a single run of indels), or the next
+            // column has no stored events (continue on the suffix)
+            bool cont = false;
+            {
+                const int rem = lim - steps;
+                if (rem > 0 && !(i == n_w && j == m_w)) {
+                    if (i == n_w || j == m_w) {
+                        const int op = i == n_w ? 2 : 3;
+                        const int left = i == n_w ? m_w - j : n_w - i;
+                        if (d != left)
+                            status = kStInternal | (i == n_w ? kDetBudgetI : kDetBudgetD);
+                        const int k = min(rem, left);
+                        i += op != 2 ? k : 0;
+                        j += op != 3 ? k : 0;
+                        d -= k;
+                        dist += k;
+                        steps += k;
+                        emit(op, k);
+                    } else {
+                        cont = true;
+                    }
+                }
+            }
+            c_reads += reads;
             if (cont && status == 0) {
                 // the window continues on the suffix t[i:n_w) x p[j:m_w)
                 toff += i;
@@ -869,12 +898,21 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         }
         __syncwarp();
         ph_tb += clock64() - ck2;
+        if (P.phase_cycles) ph_trips += warp_max(tb_trip);
     }
-    if (P.phase_cycles && lane == 0) {
-        atomicAdd(P.phase_cycles + 0, ph_setup);
-        atomicAdd(P.phase_cycles + 1, ph_dc);
-        atomicAdd(P.phase_cycles + 2, ph_tb);
-        atomicAdd(P.phase_cycles + 3, ph_it);
+    if (P.phase_cycles) {
+        ph_steps = __reduce_add_sync(kFull, static_cast<unsigned>(ph_steps));
+        ph_tbn = __reduce_add_sync(kFull, static_cast<unsigned>(ph_tbn));
+        if (lane == 0) {
+            atomicAdd(P.phase_cycles + 0, ph_setup);
+            atomicAdd(P.phase_cycles + 1, ph_dc);
+            atomicAdd(P.phase_cycles + 2, ph_tb);
+            atomicAdd(P.phase_cycles + 3, ph_it);
+            atomicAdd(P.phase_cycles + 4, ph_act);
+            atomicAdd(P.phase_cycles + 5, ph_trips);
+            atomicAdd(P.phase_cycles + 6, ph_steps);
+            atomicAdd(P.phase_cycles + 7, ph_tbn);
+        }
     }
 }
 
