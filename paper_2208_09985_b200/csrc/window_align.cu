@@ -19,6 +19,11 @@ template <int L> struct KCfg;
 template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4; };
 template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4; };
 template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
+// DC chunks per state-machine iteration (traceback batching, see the main loop)
+#ifndef SG_SUBCHUNKS
+#define SG_SUBCHUNKS 2
+#endif
+constexpr int kSubChunks = SG_SUBCHUNKS;
 // (R = 4: sweep groups are aligned to 4-column text-code words; C % 4 == 0.)
 
 // Shared memory of one warp, in 32-bit words:
@@ -327,7 +332,8 @@ template <int L, int R, int C, int MODE, bool DRAIN>
 __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const LaneMem<L>& M,
                                             uint32_t codes4, uint32_t codes4n, int col_top,
                                             uint32_t two, uint32_t one, int g0, bool z0, int n_w,
-                                            uint32_t keep_old, int r0, int p0, int& fr) {
+                                            uint32_t keep_old, uint32_t lv, int r0, int p0,
+                                            int& fr) {
     static_assert(R == 4, "groups are aligned to 4-column text-code words");
     constexpr int WB = 32 * L;
     constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
@@ -337,7 +343,7 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
     uint32_t* pbg = M.bnd + (colf0 + 4) * 32 * L;
     uint32_t* pxg = M.xy + colf0 * 64 * L;
     if (CAP) {  // earlier chunks' events of step 0's finished column
-        const uint32_t* po = M.xy + xslot<C>(colf0, n_w) * 64 * L;
+        const uint32_t* po = SLOW ? M.xy + xslot<C>(colf0, n_w) * 64 * L : pxg;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
             F.ox[l] = po[l];
@@ -350,7 +356,7 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
         uint32_t pm0[L], north0[L];                                                          \
         _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
             pm0[l] = F.pmn[l];                                                               \
-            north0[l] = F.nbr[(U)][l] | ~keep_old; /* first chunk: R[.][-1] = ones */       \
+            north0[l] = (F.nbr[(U)][l] | ~keep_old) & lv; /* first chunk: R[.][-1] = ones */\
         }                                                                                    \
         {   /* prefetch: parked row one group ahead, pattern mask of the next column */     \
             const uint32_t* src = DRAIN ? M.bnd : nbg - ((U) + 4) * 32 * L;                  \
@@ -393,29 +399,32 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
 
 // One chunk of rows d0..d0+R-1 over columns n_w-1..0 (n_w = 0: idle lane).
 // Returns the first row r of the chunk with bit j=0 of R[0][d0+r] clear, or -1.
+// A lane with live == false sweeps along with all-zero rows: it produces no
+// events and rewrites its stored events unchanged (its traceback is pending).
 template <int L, int R, int C>
-__device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, uint32_t two,
-                                        uint32_t one, const LaneMem<L>& M) {
+__device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int n_max,
+                                        uint32_t two, uint32_t one, const LaneMem<L>& M) {
     constexpr int WB = 32 * L;
     static_assert(R == 4 && WB % R == 0 && C % R == 0, "R = 4 groups aligned to C");
+    const uint32_t lv = live ? ~0u : 0u;
     Sweep<L, R> S;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int d = d0 + r;
 #pragma unroll
         for (int l = 0; l < L; ++l) {
-            S.v[r][l] = init_limb<L>(d, l);
-            S.dg[r][l] = init_limb<L>(d - 1, l);
+            S.v[r][l] = init_limb<L>(d, l) & lv;
+            S.dg[r][l] = init_limb<L>(d - 1, l) & lv;
             S.pmq[r][l] = ~0u;
             S.acc[r][0][l] = S.acc[r][1][l] = 0u;
         }
         // I(n, d) = shl1(R[n][d-1], [d == 0]) with R[n][-1] = ones
-        S.ic[r] = d == 0 ? ~0u : (init_limb<L>(d - 1, 0) << 1);
+        S.ic[r] = (d == 0 ? ~0u : (init_limb<L>(d - 1, 0) << 1)) & lv;
     }
     const int tsteps = ((n_max + R - 1) / R) * R;
     const int S0 = tsteps - 1;
-    const bool z0 = d0 == 0;
-    const uint32_t keep_old = d0 > 0 ? ~0u : 0u;
+    const bool z0 = d0 == 0 && live;
+    const uint32_t keep_old = d0 > 0 || !live ? ~0u : 0u;
     // Virtual columns >= n_w of the parked row hold R[n][d0-1].
     if (d0 > 0)
         for (int c = n_w; c <= S0; ++c)
@@ -446,19 +455,19 @@ __device__ __forceinline__ int dc_chunk(int n_w, int m_w, int d0, int n_max, uin
         }
         if (mode == kIn)
             sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
-                                             n_w, keep_old, r0, p0, fr);
+                                             n_w, keep_old, lv, r0, p0, fr);
         else if (mode == kOut)
             sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                              z0, n_w, keep_old, r0, p0, fr);
+                                              z0, n_w, keep_old, lv, r0, p0, fr);
         else
             sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                               z0, n_w, keep_old, r0, p0, fr);
+                                               z0, n_w, keep_old, lv, r0, p0, fr);
         codes4 = codes4n;
     }
     // drain: rows 1..R-1 finish (row 0 has just left column 0)
     if (!top_bit<L, R>(S, 0, r0, p0)) fr = 0;
     sweep_group<L, R, C, kSlow, true>(S, F, M, codes4, codes4, -1, two, one,
-                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, r0, p0, fr);
+                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, lv, r0, p0, fr);
     return fr;
 }
 
@@ -767,24 +776,28 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
         __syncwarp();
         const long long ck1 = clock64();
 
-        // ------------------------------------------------ DC: one chunk
-        const int n_max = warp_max(in_dc ? n_w : 0);
-        const int fr = dc_chunk<L, R, C>(in_dc ? n_w : 0, m_w, d0, n_max, two, one, lmem);
+        // ------------------------------------------------ DC chunks + d_opt detection
+        // Up to kSubChunks chunks of R rows before the traceback phase, so
+        // that more lanes reach it together; solved lanes sweep idle.
+        bool solved = false;
+        for (int sub = 0; sub < kSubChunks; ++sub) {
+            const bool act = in_dc && !solved;
+            if (sub > 0 && !__any_sync(kFull, act)) break;
+            const int n_max = warp_max(act ? n_w : 0);
+            const int fr = dc_chunk<L, R, C>(act ? n_w : 0, act, m_w, d0, n_max, two, one, lmem);
+            ++ph_it;
+            ph_act += __popc(__ballot_sync(kFull, act));
+            if (act) {
+                if (found_d < 0 && fr >= 0) found_d = d0 + fr;
+                const bool seg_et = P.et || !first_seg;
+                solved = seg_et ? found_d >= 0 : (d0 + R > W);
+                if (!solved) d0 += R;
+            }
+        }
         __syncwarp();
         const long long ck2 = clock64();
         ph_setup += ck1 - ck0;
         ph_dc += ck2 - ck1;
-        ++ph_it;
-        ph_act += __popc(__ballot_sync(kFull, in_dc));
-
-        // ------------------------------------------------ d_opt detection
-        bool solved = false;
-        if (in_dc) {
-            if (found_d < 0 && fr >= 0) found_d = d0 + fr;
-            const bool seg_et = P.et || !first_seg;
-            solved = seg_et ? found_d >= 0 : (d0 + R > W);
-            if (!solved) d0 += R;
-        }
 
         // ------------------------------------------------ TB + advance
         int tb_trip = 0;
