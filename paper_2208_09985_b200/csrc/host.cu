@@ -549,9 +549,16 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     const int wpb = sgk::k1_warps_per_block(rc.L);
-    long long grid = static_cast<long long>(st.sms) * blocks_per_sm;
-    const long long need = (n + 32LL * wpb - 1) / (32LL * wpb);
-    grid = std::max(1LL, std::min(grid, need));
+    // Each lane aligns whole pairs one after another, so a batch takes about
+    // ceil(n / lanes) pair-times. Use the fewest lanes that keep that number of
+    // rounds (fewer warps per SM run each round faster).
+    const long long max_grid = static_cast<long long>(st.sms) * blocks_per_sm;
+    const long long max_lanes = max_grid * wpb * 32;
+    const long long rounds = std::max(1LL, (static_cast<long long>(n) + max_lanes - 1) / max_lanes);
+    const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
+    long long grid = (lanes_needed + 32LL * wpb - 1) / (32LL * wpb);
+    if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
+    grid = std::max(1LL, std::min(grid, max_grid));
     st.grid = grid;
     st.lanes = grid * wpb * 32;
     st.bnd.ensure(sgk::bnd_scratch_bytes(rc.L, grid * wpb));

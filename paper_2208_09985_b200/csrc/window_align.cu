@@ -16,9 +16,9 @@ constexpr unsigned kFull = 0xffffffffu;
 // range, wider windows continue as a new segment), WARPS warps per block
 // (warps are independent; blocks only share an SM).
 template <int L> struct KCfg;
-template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4; };
-template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4; };
-template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2; };
+template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4, MINB = 2; };
+template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4, MINB = 3; };
+template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2, MINB = 1; };
 // DC chunks per state-machine iteration (traceback batching, see the main loop)
 #ifndef SG_SUBCHUNKS
 #define SG_SUBCHUNKS 2
@@ -28,13 +28,14 @@ constexpr int kSubChunks = SG_SUBCHUNKS;
 
 // Shared memory of one warp, in 32-bit words:
 //   txt [WB/8][32] u64   text codes (1 byte per column, 4 = non-ACGT / virtual)
-//   xy  [C+1][2][32][L]  traceback events X / Y per column (column C = dummy)
+//   xy  [C+1][32][2]     traceback events X / Y per column, 32-bit band around
+//                        the diagonal (band_base); column C = dummy
 //   pm  [5][32][L]       pattern masks per code (code 4: all ones)
 //   sq  [6L+4][32]       packed text (2L+1 words), pattern (2L+1), text N (L+1),
 //                        pattern N (L+1) of the current segment, for traceback
 template <int L> __host__ __device__ constexpr int txt_words() { return (32 * L / 4 + 2) * 32; }
 template <int L> __host__ __device__ constexpr int xy_words() {
-    return (KCfg<L>::C + 1) * 2 * 32 * L;
+    return (KCfg<L>::C + 1) * 2 * 32;
 }
 template <int L> __host__ __device__ constexpr int pm_words() { return 5 * L * 32; }
 // words of packed text / pattern staged per lane: the window plus the reach
@@ -173,6 +174,34 @@ template <int L> __device__ __forceinline__ uint32_t init_limb(int d, int l) {
     return z >= 32 ? 0u : (~0u << z);
 }
 
+// Traceback event band. Column i keeps the events of the 32 logical positions
+// q in [L*P, L*P + 32), P = band_base(i): bits p in [P, P + 32/L) of every limb,
+// centred on the diagonal q = i + off. Columns share P in blocks
+// {4k-1 .. 4k+2} (the columns one sweep group finishes). A traceback path that
+// leaves the band continues as a new segment (the suffix distances do not
+// depend on where the segment starts).
+template <int L> __device__ __forceinline__ int band_base(int i, int off) {
+    if (L == 1) return 0;
+    constexpr int SH = L == 2 ? 1 : 2;
+    const int P = (((i + 1) & ~3) + off - 16) >> SH;
+    return min(max(P, 0), 32 - 32 / L);
+}
+
+// The band word of a full event vector: limb r's bits p in [P, P + 32/L) at
+// band bits 31 - (32/L) r - (p - P). mul = 1 << P (an IMAD per limb).
+template <int L>
+__device__ __forceinline__ uint32_t band_word(const uint32_t (&a)[L], uint32_t mul) {
+    if constexpr (L == 1) {
+        return a[0];
+    } else if constexpr (L == 2) {
+        return __byte_perm(a[0] * mul, a[1] * mul, 0x3276);
+    } else {
+        const uint32_t u = __byte_perm(a[0] * mul, a[1] * mul, 0x3700);
+        const uint32_t v = __byte_perm(a[2] * mul, a[3] * mul, 0x0037);
+        return __byte_perm(u, v, 0x3254);
+    }
+}
+
 __device__ __forceinline__ int warp_max(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
@@ -292,13 +321,13 @@ __device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0,
 // Per-lane views of the warp's shared memory and parked-row scratch.
 //   bnd (stride 32L words): slot c + 4 = column c (slots 0..3 pad the
 //   one-group-ahead prefetch past column 0), WB + 4 = dummy store target.
-//   xy (stride 64L words per column, +32L for Y): column C is the dummy.
+//   xy (stride 64 words per column, X / Y adjacent): column C is the dummy.
 //   txt: 4 text codes per word, word w + 1 = columns 4w..4w+3 (word 0 pads
 //   column -1 with code 4).
 template <int L>
 struct LaneMem {
     uint32_t* bnd;        // + lane * L
-    uint32_t* xy;         // + lane * L
+    uint32_t* xy;         // + lane * 2
     const uint32_t* pm;   // + lane * L
     const uint32_t* txt;  // + lane
 };
@@ -310,7 +339,7 @@ template <int L>
 struct Pref {
     uint32_t nbr[4][L];
     uint32_t pmn[L];
-    uint32_t ox[L], oy[L];
+    uint32_t ox, oy;
 };
 
 template <int C>
@@ -333,7 +362,7 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
                                             uint32_t codes4, uint32_t codes4n, int col_top,
                                             uint32_t two, uint32_t one, int g0, bool z0, int n_w,
                                             uint32_t keep_old, uint32_t lv, int r0, int p0,
-                                            int& fr) {
+                                            int off, int& fr) {
     static_assert(R == 4, "groups are aligned to 4-column text-code words");
     constexpr int WB = 32 * L;
     constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
@@ -341,14 +370,14 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
     const uint32_t* nbg = M.bnd + (col_top + 4) * 32 * L;
     const int colf0 = col_top + R - 1;
     uint32_t* pbg = M.bnd + (colf0 + 4) * 32 * L;
-    uint32_t* pxg = M.xy + colf0 * 64 * L;
-    if (CAP) {  // earlier chunks' events of step 0's finished column
-        const uint32_t* po = SLOW ? M.xy + xslot<C>(colf0, n_w) * 64 * L : pxg;
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-            F.ox[l] = po[l];
-            F.oy[l] = po[32 * L + l];
-        }
+    uint32_t* pxg = M.xy + colf0 * 64;
+    uint32_t mul = 1;
+    if (CAP) {  // earlier chunks' events of step 0's finished column; band of the group
+        const uint2 o = *reinterpret_cast<const uint2*>(SLOW ? M.xy + xslot<C>(colf0, n_w) * 64
+                                                               : pxg);
+        F.ox = o.x;
+        F.oy = o.y;
+        mul = 1u << band_base<L>(colf0, off);
     }
 #define SG_STEP(U)                                                                           \
     if (!DRAIN || (U) + 1 < R) {                                                             \
@@ -370,24 +399,22 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
             constexpr int SL = ((U) + 1) & (R - 1);                                          \
             const int colf = colf0 - (U);                                                    \
             uint32_t* pb = pbg - (U) * 32 * L;                                               \
-            uint32_t* px = pxg - (U) * 64 * L;                                               \
+            uint32_t* px = pxg - (U) * 64;                                                   \
             if (SLOW) {                                                                      \
                 pb = M.bnd + (colf >= 0 && colf < n_w ? colf + 4 : WB + 4) * 32 * L;         \
-                px = M.xy + xslot<C>(colf, n_w) * 64 * L;                                    \
+                px = M.xy + xslot<C>(colf, n_w) * 64;                                        \
             }                                                                                \
             _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];             \
             if (CAP) {                                                                       \
-                _Pragma("unroll") for (int l = 0; l < L; ++l) {                              \
-                    px[l] = (F.ox[l] & keep_old) | S.acc[SL][0][l];                          \
-                    px[32 * L + l] = (F.oy[l] & keep_old) | S.acc[SL][1][l];                 \
-                }                                                                            \
+                uint2 o;                                                                     \
+                o.x = (F.ox & keep_old) | band_word<L>(S.acc[SL][0], mul);                   \
+                o.y = (F.oy & keep_old) | band_word<L>(S.acc[SL][1], mul);                   \
+                *reinterpret_cast<uint2*>(px) = o;                                           \
                 if ((U) + 1 < R) { /* next step's column; groups reload at their start */   \
-                    const uint32_t* po = SLOW ? M.xy + xslot<C>(colf - 1, n_w) * 64 * L      \
-                                              : px - 64 * L;                                 \
-                    _Pragma("unroll") for (int l = 0; l < L; ++l) {                          \
-                        F.ox[l] = po[l];                                                     \
-                        F.oy[l] = po[32 * L + l];                                            \
-                    }                                                                        \
+                    const uint2 n = *reinterpret_cast<const uint2*>(                         \
+                        SLOW ? M.xy + xslot<C>(colf - 1, n_w) * 64 : px - 64);               \
+                    F.ox = n.x;                                                              \
+                    F.oy = n.y;                                                              \
                 }                                                                            \
             }                                                                                \
         }                                                                                    \
@@ -455,26 +482,26 @@ __device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int
         }
         if (mode == kIn)
             sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
-                                             n_w, keep_old, lv, r0, p0, fr);
+                                             n_w, keep_old, lv, r0, p0, off, fr);
         else if (mode == kOut)
             sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                              z0, n_w, keep_old, lv, r0, p0, fr);
+                                              z0, n_w, keep_old, lv, r0, p0, off, fr);
         else
             sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                               z0, n_w, keep_old, lv, r0, p0, fr);
+                                               z0, n_w, keep_old, lv, r0, p0, off, fr);
         codes4 = codes4n;
     }
     // drain: rows 1..R-1 finish (row 0 has just left column 0)
     if (!top_bit<L, R>(S, 0, r0, p0)) fr = 0;
     sweep_group<L, R, C, kSlow, true>(S, F, M, codes4, codes4, -1, two, one,
-                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, lv, r0, p0, fr);
+                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, lv, r0, p0, off, fr);
     return fr;
 }
 
 // ------------------------------------------------------------------ K1
 
 template <int L>
-__global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
+__global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
     k1_window_align(const AlignParams P) {
     constexpr int R = KCfg<L>::R, C = KCfg<L>::C, WB = 32 * L, NW = 2 * L;
     extern __shared__ uint32_t smem[];
@@ -482,7 +509,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     const int wib = threadIdx.x >> 5;
     uint32_t* const wbase = smem + wib * warp_smem_words<L>();
     uint64_t* const txt = reinterpret_cast<uint64_t*>(wbase);   // [WB/8][32]
-    uint32_t* const xy = wbase + txt_words<L>();                 // [C+1][2][32][L]
+    uint32_t* const xy = wbase + txt_words<L>();                 // [C+1][32][2]
     uint32_t* const pmv = xy + xy_words<L>();                    // [5][32][L]
     uint32_t* const sq = pmv + pm_words<L>();                    // [6L+4][32]
     constexpr int PFW = pf_words<L>();
@@ -493,7 +520,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
     uint32_t* const bnd = P.bnd + gwarp * (WB + 5) * 32 * L;    // [WB+5][32][L]
     const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
-    const LaneMem<L> lmem{bnd + lane * L, xy + lane * L, pmv + lane * L,
+    const LaneMem<L> lmem{bnd + lane * L, xy + lane * 2, pmv + lane * L,
                           reinterpret_cast<const uint32_t*>(txt) + lane};
 
 #pragma unroll
@@ -837,10 +864,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS)
                 const int rem = lim - steps;
                 if (rem == 0 || i == n_w || j == m_w || i >= C) break;
                 // event words of (i, j) and the match-run words load together
+                const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
+                const uint32_t xw = ev.x, yw = ev.y;
                 const unsigned q = static_cast<unsigned>(j + off);
-                const uint32_t* ev = xy + (i * 64 + lane) * L + q % L;
-                const uint32_t xw = ev[0], yw = ev[32 * L];
-                const uint32_t bit = 0x80000000u >> (q / L);
+                const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
+                if (static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
+                const uint32_t bit = 0x80000000u >> ((32 / L) * (q % L) + dp);
                 const int run = match_run(i, j);
                 const bool ed = run == 0;  // the other bounds are >= 1 here
                 const int k = ed ? 1 : min(min(run, rem), min(min(n_w - i, m_w - j), C - i));
