@@ -62,12 +62,15 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
+    alt = os.environ.get("SG_LIB_OVERRIDE")  # development aid: A/B against another build
+    if alt:
+        build_if_missing = False
     if build_if_missing and _build._stale():
         _build.build()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"scrooge_b200 CUDA library missing: {LIB_PATH} "
                           "(run python -m paper_2208_09985_b200.build)")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(alt or LIB_PATH)
     P = C.POINTER
     L.sg_abi_version.restype = C.c_int
     L.sg_device_count.restype = C.c_int
