@@ -205,6 +205,20 @@ def reference_sample_size(threads: int) -> int:
     return int(min(100000, max(200, threads * 1200)))
 
 
+def traffic_bytes(pairs):
+    """DRAM bytes (read + write) of one K1 launch, from the committed ncu --set full
+    capture of the same workload (profiles/k1_traffic.json); None if it does not
+    match this run's batch size."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            t = json.load(f)
+        if f"{pairs} pairs" not in t["workload"]:
+            return None
+        return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cpu_baseline(threads: int):
     n = reference_sample_size(threads)
     r = run_reference_sample(n, threads)
@@ -366,7 +380,8 @@ def main_ours(args):
                        "resident_lanes": info["lanes"]},
             "roofline": {"bound": "int_alu", "achieved": round(achieved / 1e12, 3),
                          "peak": round(peak / 1e12, 3), "unit": "Tops/s (int32 lane-ops)",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_bytes(pairs),
+                         "traffic_unit": "DRAM bytes per K1 launch (ncu, profiles/k1_traffic.json)",
                          "alg_ops_per_launch": alg_ops, "cells_computed": cells,
                          "k1_ms": round(sum(k1_ms) / len(k1_ms), 3),
                          "r_alu_ops_per_clk_per_sm": round(r_alu.value, 2),
