@@ -472,6 +472,8 @@ struct RunConfig {
 };
 
 unsigned long long* g_phase_buf = nullptr;  // diagnostics (SG_PHASE_CYCLES=1)
+unsigned long long* g_warp_times = nullptr;  // diagnostics (SG_WARP_TIMES=1)
+int g_warp_count = 0;
 
 RunConfig run_config(const sg_config* c) {
     RunConfig r;
@@ -558,6 +560,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
     long long grid = (lanes_needed + 32LL * wpb - 1) / (32LL * wpb);
     if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
+    if (const char* e = getenv("SG_BLOCKS")) grid = std::max(1LL, std::min(atoll(e), max_grid));
     grid = std::max(1LL, std::min(grid, max_grid));
     st.grid = grid;
     st.lanes = grid * wpb * 32;
@@ -589,6 +592,17 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.bnd = st.bnd.as<uint32_t>();
     p.next_pair = st.next_pair.as<unsigned int>();
     p.phase_cycles = nullptr;
+    p.warp_times = nullptr;
+    if (const char* e = getenv("SG_WARP_TIMES")) {  // diagnostics
+        if (e[0] == '1') {
+            static unsigned long long* wbuf = nullptr;
+            if (!wbuf) SG_CUDA_CHECK(cudaMalloc(&wbuf, 8 * 3 * 8192));
+            SG_CUDA_CHECK(cudaMemsetAsync(wbuf, 0, 8 * 3 * 8192, st.stream));
+            p.warp_times = wbuf;
+            g_warp_times = wbuf;
+            g_warp_count = static_cast<int>(grid * wpb);
+        }
+    }
     if (const char* e = getenv("SG_PHASE_CYCLES")) {
         if (e[0] == '1') {
             static unsigned long long* dbuf = nullptr;
@@ -1122,6 +1136,13 @@ void sg_session_destroy(sg_session* s) { delete s; }
  * SG_PHASE_CYCLES=1 (setup, DC, TB+advance, iterations, lanes in DC, TB loop
  * trips, TB lane-steps, TB entries). Not part of the ABI
  * header. */
+int sg_debug_warp_times(unsigned long long* out, int cap) {
+    if (!g_warp_times) return -1;
+    const int n = std::min(cap, g_warp_count);
+    cudaMemcpy(out, g_warp_times, 24 * static_cast<size_t>(n), cudaMemcpyDeviceToHost);
+    return n;
+}
+
 int sg_debug_phase_cycles(unsigned long long* out8) {
     if (!g_phase_buf) return -1;
     cudaMemcpy(out8, g_phase_buf, 64, cudaMemcpyDeviceToHost);

@@ -772,6 +772,11 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         return __clz(__brev(x)) >> 1;  // 16 when all 16 bases match
     };
 
+    if (P.warp_times && lane == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.warp_times[gwarp * 3] = t;
+    }
     bool need_pair = true, need_window = false, need_load = false;
     unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0, ph_act = 0, ph_trips = 0,
                        ph_steps = 0, ph_tbn = 0;
@@ -941,6 +946,13 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         __syncwarp();
         ph_tb += clock64() - ck2;
         if (P.phase_cycles) ph_trips += warp_max(tb_trip);
+    }
+    if (P.warp_times && lane == 0) {  // diagnostics: when each warp leaves, on which SM
+        unsigned long long t, smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned*>(&smid)));
+        P.warp_times[gwarp * 3 + 1] = t;
+        P.warp_times[gwarp * 3 + 2] = smid & 0xFFFFFFFFull;
     }
     if (P.phase_cycles) {
         ph_steps = __reduce_add_sync(kFull, static_cast<unsigned>(ph_steps));

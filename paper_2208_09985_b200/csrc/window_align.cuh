@@ -65,7 +65,8 @@ struct AlignParams {
     uint32_t* scratch;        // run bytes, (op << 6) | (len - 1)
     uint32_t* bnd;            // parked rows: per warp [32L + 1 columns][32 lanes][L]
     unsigned int* next_pair;  // work queue head
-    unsigned long long* phase_cycles;  // optional [4]: setup, DC, TB, iterations (diagnostics)
+    unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
+    unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
 
 // Launch K1 for limb count L (W <= 32L). Returns cudaError_t as int.
