@@ -436,8 +436,8 @@ class Session:
 # ----------------------------------------------------------------- reference-shaped API
 
 def _outcome(res: Results, k: int) -> PairOutcome:
-    return PairOutcome(True, int(res.distance[k]), res.cigar(k), int(res.windows[k]),
-                       res.pair_counters(k))
+    return PairOutcome(bool(res.found[k]), int(res.distance[k]), res.cigar(k),
+                       int(res.windows[k]), res.pair_counters(k))
 
 
 def align(text, pattern, config: Optional[AlignerConfig] = None) -> AlignmentResult:

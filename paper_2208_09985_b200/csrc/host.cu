@@ -238,20 +238,32 @@ int validate_cfg(const sg_config* c) {
     if (c->single_window && (c->k_single < 0 || c->k_single > 1024))
         return set_error(SG_CONFIG, "k out of range: %d", c->k_single);
     // GPU-path limits (SURVEY §8(b) semantic gaps)
-    if (c->single_window)
-        return set_error(SG_CONFIG, "single-window mode is not implemented on the GPU path");
-    if (!limbs_for(c->W))
+    if (!c->single_window && !limbs_for(c->W))
         return set_error(SG_CONFIG, "the GPU path supports W <= 128, got W=%d", c->W);
     return SG_OK;
 }
 
-int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl) {
+constexpr int64_t kMaxSingle = 1024;     // BitVector::kMaxBits (bitvec.hpp:29)
+constexpr int64_t kMaxSingleGpu = 128;   // longest single window of the GPU path
+
+int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl, const sg_config* c) {
     for (int64_t k = 0; k < n; ++k) {
         if (tl[k] <= 0 || pl[k] <= 0)  // batch.cpp:18-25
             return set_error(SG_INPUT, "pair '%lld': empty sequence", static_cast<long long>(k));
         if (tl[k] + pl[k] > (int64_t{1} << 30))
             return set_error(SG_INPUT, "pair '%lld': sequence too long for one GPU pair slot",
                              static_cast<long long>(k));
+        if (c->single_window) {
+            // aligner.cpp:92-94; run_batch reports it as an input error (batch.cpp:94-97)
+            if (tl[k] > kMaxSingle || pl[k] > kMaxSingle)
+                return set_error(SG_INPUT,
+                                 "pair '%lld': single-window mode requires sequences of at most "
+                                 "1024 characters", static_cast<long long>(k));
+            if (tl[k] > kMaxSingleGpu || pl[k] > kMaxSingleGpu)
+                return set_error(SG_CONFIG,
+                                 "pair '%lld': single-window mode on the GPU path supports "
+                                 "sequences of at most 128 characters", static_cast<long long>(k));
+        }
     }
     return SG_OK;
 }
@@ -468,16 +480,25 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first) {
 }
 
 struct RunConfig {
-    int L, W, O, et, policy;
+    int L, W, O, et, policy, single, k_single;
 };
 
 unsigned long long* g_phase_buf = nullptr;  // diagnostics (SG_PHASE_CYCLES=1)
 unsigned long long* g_warp_times = nullptr;  // diagnostics (SG_WARP_TIMES=1)
 int g_warp_count = 0;
 
-RunConfig run_config(const sg_config* c) {
+// Single-window mode sizes the vectors by the longest sequence of the batch.
+RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = nullptr,
+                     const int64_t* pl = nullptr) {
     RunConfig r;
     r.L = limbs_for(c->W);
+    r.single = c->single_window ? 1 : 0;
+    r.k_single = c->k_single;
+    if (r.single) {
+        int64_t mx = 1;
+        for (int64_t k = 0; k < n; ++k) mx = std::max(mx, std::max(tl[k], pl[k]));
+        r.L = limbs_for(static_cast<int>(mx));
+    }
     r.W = c->W;
     r.O = c->O;
     r.et = c->early_termination ? 1 : 0;
@@ -582,6 +603,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.et = rc.et;
     p.policy = rc.policy;
     p.two = 2;
+    p.single = rc.single;
+    p.k_single = rc.k_single;
     p.distance = st.distance.as<int32_t>();
     p.windows = st.windows.as<int32_t>();
     p.status = st.status.as<int32_t>();
@@ -700,7 +723,7 @@ void scatter_small(sg_results* out, int64_t base, int64_t n, int64_t run_base, c
     for (int64_t k = 0; k < n; ++k) {
         out->distance[base + k] = dist[k];
         out->windows[base + k] = win[k];
-        out->found[base + k] = 1;
+        out->found[base + k] = dist[k] >= 0;  // single window: D > k is "not found"
         out->cigar_off[base + k] = run_base + doff[k];
     }
     out->cigar_off[base + n] = run_base + doff[n];
@@ -728,7 +751,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     if (!in || in->n_pairs < 0) return set_error(SG_INPUT, "null or negative pair batch");
     const int64_t n = in->n_pairs;
     if (n > INT32_MAX) return set_error(SG_INPUT, "too many pairs in one batch");
-    rc = validate_lengths(n, in->text_len, in->pat_len);
+    rc = validate_lengths(n, in->text_len, in->pat_len, cfg);
     if (rc) return rc;
     int dev_default = 0;
     if (!devices || n_devices < 1) {
@@ -741,7 +764,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     for (int d = 0; d < n_devices; ++d)
         if (devices[d] < 0 || devices[d] >= count)
             return set_error(SG_CONFIG, "bad device index %d", devices[d]);
-    const RunConfig rcfg = run_config(cfg);
+    const RunConfig rcfg = run_config(cfg, n, in->text_len, in->pat_len);
     const size_t nd = static_cast<size_t>(n_devices);
 
     // K5: contiguous shards with balanced cost (text + pattern length)
@@ -947,7 +970,7 @@ int sg_align_batch(const sg_config* cfg, const sg_pairs* pairs, const int* devic
     int rc = validate_cfg(cfg);
     if (rc) return rc;
     if (!pairs || pairs->n_pairs < 0) return set_error(SG_INPUT, "null or negative pair batch");
-    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len);
+    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len, cfg);
     if (rc) return rc;
     try {
         Packed pk;
@@ -1055,14 +1078,14 @@ int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int de
     if (rc) return rc;
     if (!pairs || pairs->n_pairs < 0 || pairs->n_pairs > INT32_MAX)
         return set_error(SG_INPUT, "bad pair batch");
-    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len);
+    rc = validate_lengths(pairs->n_pairs, pairs->text_len, pairs->pat_len, cfg);
     if (rc) return rc;
     if (sg_device_count() <= device || device < 0)
         return set_error(SG_CUDA, "no CUDA device %d (the GPU path has no CPU fallback)", device);
     auto s = std::make_unique<sg_session>();
     try {
         s->cfg = *cfg;
-        s->rc = run_config(cfg);
+        s->rc = run_config(cfg, pairs->n_pairs, pairs->text_len, pairs->pat_len);
         s->st.init(device);
         s->n = pairs->n_pairs;
         bool mixed = false;

@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
 
     const int W = P.W;
     const int step_limit = W - P.O;
+    const int K = P.single ? P.k_single : W;  // edit budget: rows 0..K
 
     // ---- lane state ----
     int pair = -1;
@@ -691,9 +692,10 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             }
             return false;
         }
-        const bool fin = n_rem <= W && m_rem <= W;
-        n_w = min(W, n_rem);
-        m_w = min(W, m_rem);
+        // single-window mode (aligner.cpp:87-112): the whole pair is one final window
+        const bool fin = P.single || (n_rem <= W && m_rem <= W);
+        n_w = P.single ? n_rem : min(W, n_rem);
+        m_w = P.single ? m_rem : min(W, m_rem);
         limit = fin ? -1 : step_limit;
         first_seg = true;
         d0 = 0;
@@ -716,7 +718,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             c[2] = c_reads;
             c[3] = c_rows;
             c[4] = c_cells;
-            c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(W + 1);
+            c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
             c[6] = c_bequiv;
         }
     };
@@ -820,9 +822,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             ++ph_it;
             ph_act += __popc(__ballot_sync(kFull, act));
             if (act) {
-                if (found_d < 0 && fr >= 0) found_d = d0 + fr;
+                if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
                 const bool seg_et = P.et || !first_seg;
-                solved = seg_et ? found_d >= 0 : (d0 + R > W);
+                solved = seg_et ? (found_d >= 0 || d0 + R > K) : (d0 + R > K);
                 if (!solved) d0 += R;
             }
         }
@@ -834,10 +836,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         // ------------------------------------------------ TB + advance
         int tb_trip = 0;
         if (in_dc && solved) {
-            if (found_d < 0) status = kStInternal | kDetNoStep;  // aligner.cpp:69-70
+            // single window with D(0, 0) > k: not found (batch.cpp:57-62)
+            const bool not_found = P.single && found_d < 0;
+            if (found_d < 0 && !not_found) status = kStInternal | kDetNoStep;  // aligner.cpp:69-70
             if (first_seg) {
                 // reference counters for this logical window (dp.cpp:23-37,58-75,225-228)
-                const int rows_ref = P.et ? found_d + 1 : W + 1;
+                const int rows_ref = P.et && found_d >= 0 ? found_d + 1 : K + 1;
                 int pol = P.policy;
                 if (limit < 0 && pol == 2) pol = 1;  // final window: DENT -> SENE
                 int keep_cols = n_w + 1, keep_bits = m_w;
@@ -850,10 +854,17 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                 c_writes += static_cast<unsigned long long>(rows_ref) * keep_cols * slots;
                 c_rows += rows_ref;
                 c_cells += static_cast<unsigned long long>(rows_ref) * n_w;
-                c_bequiv += 3ull * (n_w + 1) * static_cast<unsigned long long>(W + 1) * m_w;
+                c_bequiv += 3ull * (n_w + 1) * static_cast<unsigned long long>(K + 1) * m_w;
             } else if (found_d != expect_d) {
                 status = kStInternal | kDetSegment;
             }
+            if (not_found) {
+                dist = -1;
+                ++nwin;
+                toff = n_tot;
+                poff = m_tot;
+                need_window = true;
+            } else {
             // GenASM-TB (traceback.cpp:56-113). On the path D(i,j) == d, so
             // Match <=> t_i == p_j (both ACGT) and runs of matches are taken
             // at once; at a mismatch the events pick Sub > Del > Ins.
@@ -921,7 +932,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                     }
                 }
             }
-            c_reads += reads;
+            if (!P.single) c_reads += reads;  // single window: counted before TB (aligner.cpp:98-99)
             if (cont && status == 0) {
                 // the window continues on the suffix t[i:n_w) x p[j:m_w)
                 toff += i;
@@ -942,6 +953,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                 if (nwin > window_cap) status = kStInternal | kDetWatchdog;
                 need_window = true;
             }
+            }  // found
         }
         __syncwarp();
         ph_tb += clock64() - ck2;

@@ -55,6 +55,8 @@ struct AlignParams {
     int32_t n_pairs;
     int32_t W, O, et, policy; // policy: 0 BaselineEdges, 1 SeneEntries, 2 DentTrimmed (counters)
     int32_t two;              // the constant 2 at run time (keeps the DP shift an IMAD)
+    int32_t single;           // single-window mode (aligner.cpp:87-112)
+    int32_t k_single;         // its edit budget
     // outputs
     int32_t* distance;
     int32_t* windows;

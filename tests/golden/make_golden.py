@@ -97,6 +97,36 @@ def main():
                  *cfg_flags(W, O, s, d, e)], f"cfg4_W{W}_O{O}_s{s}d{d}e{e}.tsv")
     ref(["synth", "--cfg", "5", "--count", "500", "--hash", *cfg_flags(64, 24)], "cfg5_head.tsv")
 
+    # --- single-window mode (align_single_window, proj/src/aligner.cpp:87-112;
+    #     proj/tests/test_aligner.cpp:135-161, test_harness.cpp:154-160)
+    rng = random.Random(8712)
+    single = [("acgt_acga", "ACGT", "ACGA"), ("gattaca", "GATTACA", "GATTACA"),
+              ("aaaa_cccc", "AAAA", "CCCC"), ("far", "AAAAAAAA", "CCCCCCCC"),
+              ("anmt", "ANGT", "ANGT"), ("a_t", "A", "T")]
+    for k in range(60):  # random pairs, lengths 1..128, with N
+        single.append((f"r{k}", rand_seq(rng, rng.randint(1, 128), "ACGTN" if k % 5 == 0 else "ACGT"),
+                       rand_seq(rng, rng.randint(1, 128))))
+    for k in range(40):  # related pairs (a read and its mutated copy), lengths up to 128
+        base = rand_seq(rng, rng.randint(1, 120))
+        read = list(base)
+        for _ in range(max(1, len(read) // 8)):
+            pos = rng.randrange(len(read))
+            r = rng.random()
+            if r < 0.4:
+                read[pos] = rng.choice("ACGT")
+            elif r < 0.7:
+                read.insert(pos, rng.choice("ACGT"))
+            elif len(read) > 1:
+                del read[pos]
+        single.append((f"m{k}", base, "".join(read)))
+    write_pairs("single_pairs.tsv", single)
+    single_tsv = os.path.join(HERE, "single_pairs.tsv")
+    for k in (0, 2, 3, 16, 64, 128, 1024):
+        for s, e in ((1, 1), (0, 1), (1, 0), (0, 0)):
+            ref(["align", "--input", single_tsv, "--mode", "single", "--k", str(k),
+                 "--W", "64", "--O", "33", "--sene", str(s), "--dent", "0", "--et", str(e)],
+                f"single_k{k}_s{s}e{e}.tsv")
+
 
 if __name__ == "__main__":
     sys.exit(main())

@@ -70,3 +70,24 @@ def pair_index(pid: str) -> int:
 
 def run_count(cigar: str) -> int:
     return len(re.findall(r"\d+[=XID]", cigar))
+
+
+_SINGLE = re.compile(r"single_k(\d+)_s(\d)e(\d)\.tsv$")
+
+
+def single_pairs():
+    out = {}
+    with open(os.path.join(HERE, "single_pairs.tsv")) as f:
+        for line in f:
+            pid, t, p = line.rstrip("\n").split("\t")
+            out[pid] = (t, p)
+    return out
+
+
+def single_files():
+    """(file, k_single, sene, et) of every single-window result file (dent off)."""
+    out = []
+    for path in sorted(glob.glob(os.path.join(HERE, "single_k*.tsv"))):
+        m = _SINGLE.search(path)
+        out.append((os.path.basename(path), int(m.group(1)), int(m.group(2)), int(m.group(3))))
+    return out

@@ -125,3 +125,14 @@ def test_cigar_string_helpers(sg):
     assert sg.cigar_from_string("3=1X2=3=") == [("=", 3), ("X", 1), ("=", 5)]
     with pytest.raises(sg.InputError):
         sg.cigar_from_string("3=0X")
+
+
+def test_single_window_length_limits(sg):
+    # aligner.cpp:92-94 through run_batch (batch.cpp:94-97): an input error naming the pair
+    cfg = sg.AlignerConfig(mode="single", dent=False)
+    with pytest.raises(sg.InputError, match="toolong.*at most 1024"):
+        sg.run_batch([sg.SeqPairRecord("toolong", "A" * 2000, "A" * 2000)], cfg)
+    # the GPU path's own limit: a config error, not a silent fallback
+    with pytest.raises(sg.ConfigError, match="mid.*at most 128"):
+        sg.run_batch([sg.SeqPairRecord("mid", "A" * 300, "A" * 300)], cfg)
+    cfg.validate()  # single-window configs without DENT are valid

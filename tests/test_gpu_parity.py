@@ -226,3 +226,53 @@ def test_run_batch_api_and_tsv(gpu):
     assert br.gpu_launches >= 1 and br.device_ms > 0
     with pytest.raises(sg.ConfigError):
         sg.run_batch(pairs, sg.AlignerConfig(), threads=0)
+
+
+@pytest.mark.parametrize("name,k,s,e", G.single_files())
+def test_reference_single_window(gpu, name, k, s, e):
+    # align_single_window (proj/src/aligner.cpp:87-112), run_batch's found flag
+    # (batch.cpp:47-62): exact alignments, "not found" past k, reference counters
+    sg = gpu
+    pairs = G.single_pairs()
+    rows = G.read_golden(name)
+    cfg = sg.AlignerConfig(W=64, O=33, sene=bool(s), dent=False, early_termination=bool(e),
+                           mode="single", k_single=k)
+    codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
+                                     [sg.encode_sequence(pairs[r["id"]][1]) for r in rows])
+    res = sg.align_codes(cfg, codes)
+    for j, row in enumerate(rows):
+        assert bool(res.found[j]) == (row["distance"] >= 0), row["id"]
+        if row["distance"] < 0:
+            assert int(res.distance[j]) == -1 and res.cigar_string(j) == "", row["id"]
+            assert int(res.windows[j]) == row["windows"], row["id"]
+            assert [int(x) for x in res.counters[j]] == row["counters"], row["id"]
+        else:
+            _compare(res, j, row)
+
+
+def test_single_window_run_batch_and_tsv(gpu):
+    # proj/tests/test_harness.cpp:154-160, test_aligner.cpp:135-161
+    sg = gpu
+    sw = sg.AlignerConfig(mode="single", dent=False, k_single=2)
+    far = [sg.SeqPairRecord("far", "AAAAAAAA", "CCCCCCCC")]
+    nf = sg.run_batch(far, sw)
+    assert not nf.outcomes[0].found
+    import io
+    buf = io.StringIO()
+    sg.write_batch_tsv(buf, far, nf)
+    assert buf.getvalue() == "far\t-1\t*\n"
+    cfg = sg.AlignerConfig(mode="single", dent=False, k_single=4)
+    r = sg.run_batch([sg.SeqPairRecord("a", "ACGT", "ACGA")], cfg)
+    assert r.outcomes[0].found and r.outcomes[0].distance == 1
+    assert sg.cigar_to_string(r.outcomes[0].cigar) == "3=1X"
+    rng = random.Random(46)
+    recs = []
+    for k in range(150):
+        recs.append(sg.SeqPairRecord(f"p{k}", "".join(rng.choice("ACGT") for _ in range(rng.randint(1, 64))),
+                                     "".join(rng.choice("ACGT") for _ in range(rng.randint(1, 64)))))
+    res = sg.run_batch(recs, sg.AlignerConfig(mode="single", dent=False, k_single=64))
+    for rec, po in zip(recs, res.outcomes):
+        assert po.found
+        a = O.align(O.encode(rec.text), O.encode(rec.pattern), dent=False, single_window=True,
+                    k_single=64)
+        assert po.distance == a.distance and sg.cigar_to_string(po.cigar) == a.cigar

@@ -80,3 +80,16 @@ def test_synth_matches_reference_generator_contract():
     assert len(t) == 10500 and 9000 < len(p) < 11000
     t, p = O.synth_pair(O.baseline_spec(1), 0)
     assert len(t) == 110 and p[:3] in (t[:3], p[:3])
+
+
+@pytest.mark.parametrize("name,k,s,e", G.single_files())
+def test_oracle_matches_reference_single_window(name, k, s, e):
+    # align_single_window (proj/src/aligner.cpp:87-112): found / not found past k,
+    # exact distance and CIGAR, counters taken before the traceback
+    pairs = G.single_pairs()
+    for row in G.read_golden(name):
+        t, p = pairs[row["id"]]
+        a = O.align(O.encode(t), O.encode(p), W=64, O=33, sene=s, dent=False, et=e,
+                    single_window=True, k_single=k)
+        _check_row(row, a)
+        assert a.found == (row["distance"] >= 0), row["id"]
