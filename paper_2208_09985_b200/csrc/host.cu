@@ -178,6 +178,10 @@ struct DevState {
     cudaEvent_t ev[3] = {};
     DevBuf seq, nmask, text_off, pat_off, text_len, pat_len, has_n, order;
     DevBuf distance, windows, status, out_bytes, counters, bound_off, scratch, bnd, next_pair;
+    DevBuf ready;                    // per-chunk "sequence words arrived" flags (streamed upload)
+    cudaStream_t copy = nullptr;     // H2D of the sequence words, overlapping K1
+    cudaEvent_t copy_go = nullptr;
+    int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     long long grid = 0, lanes = 0;
 
@@ -186,6 +190,8 @@ struct DevState {
         SG_CUDA_CHECK(cudaSetDevice(dev));
         SG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         SG_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        SG_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        SG_CUDA_CHECK(cudaEventCreateWithFlags(&copy_go, cudaEventDisableTiming));
         for (auto& e : ev) SG_CUDA_CHECK(cudaEventCreate(&e));
     }
     ~DevState() {
@@ -193,8 +199,10 @@ struct DevState {
         cudaSetDevice(device);
         for (DevBuf* b : {&seq, &nmask, &text_off, &pat_off, &text_len, &pat_len, &has_n, &order,
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
-                          &scratch, &bnd, &next_pair, &dense_off, &dense, &scan_tmp})
+                          &scratch, &bnd, &next_pair, &ready, &dense_off, &dense, &scan_tmp})
             b->release();
+        if (copy) cudaStreamDestroy(copy);
+        if (copy_go) cudaEventDestroy(copy_go);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         cudaStreamDestroy(stream);
@@ -467,15 +475,31 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first) {
     }
     pp.any_n = any_n;
     pp.scratch_bytes = bound;
-    pp.ordered = longest_first && n > 1;
+    pp.ordered = longest_first && n > 1 && !getenv("SG_NO_LPT");  // env: experiments
     if (pp.ordered) {
         pp.order.ensure(4 * static_cast<size_t>(n));
         int32_t* o = pp.order.as<int32_t>();
-        std::iota(o, o + n, 0);
-        std::stable_sort(o, o + n, [&](int32_t a, int32_t b) {
-            return in->text_len[s.lo + a] + in->pat_len[s.lo + a] >
-                   in->text_len[s.lo + b] + in->pat_len[s.lo + b];
-        });
+        // longest first, ties in input order: a stable LSD radix sort on the
+        // complemented length key (two 16-bit digits), O(n)
+        std::vector<uint32_t> key(static_cast<size_t>(n)), k2(static_cast<size_t>(n));
+        std::vector<int32_t> tmp(static_cast<size_t>(n));
+        for (int64_t k = 0; k < n; ++k) {
+            o[k] = static_cast<int32_t>(k);
+            key[k] = ~static_cast<uint32_t>(
+                std::min<int64_t>(in->text_len[s.lo + k] + in->pat_len[s.lo + k], 0xFFFFFFFFll));
+        }
+        for (int shift = 0; shift < 32; shift += 16) {
+            std::vector<int64_t> cnt(65537, 0);
+            for (int64_t k = 0; k < n; ++k) ++cnt[((key[k] >> shift) & 0xFFFF) + 1];
+            for (int b = 0; b < 65536; ++b) cnt[b + 1] += cnt[b];
+            for (int64_t k = 0; k < n; ++k) {
+                const int64_t dst = cnt[(key[k] >> shift) & 0xFFFF]++;
+                tmp[dst] = o[k];
+                k2[dst] = key[k];
+            }
+            std::copy(tmp.begin(), tmp.end(), o);
+            key.swap(k2);
+        }
     }
 }
 
@@ -506,22 +530,41 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
     return r;
 }
 
-int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp) {
+// Sequence words go in kChunks pieces. Streamed (one-shot calls): the pieces
+// go on the copy stream, each followed by its ready flag, while K1 already runs
+// on the main stream; a lane waits for the piece holding its pair's last word
+// (K1 fetch). Otherwise (sessions) everything is copied and flagged up front.
+constexpr int kChunks = 8;
+
+int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool streamed = false) {
     const int64_t n = pp.n;
     const sg_packed_pairs* in = s.in;
     const int64_t words = pp.word_hi - pp.word_lo;
     int64_t h2d_bytes = 0;
     const size_t seq_bytes = 4 * static_cast<size_t>(words + 24);  // K1 reads up to 12 words past a start
     st.seq.ensure(seq_bytes);
+    st.ready.ensure(4 * kChunks);
     const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 24, in->seq_words - pp.word_lo));
-    if (avail > 0) {
-        SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.p, in->seq + pp.word_lo, 4 * static_cast<size_t>(avail),
-                                      cudaMemcpyHostToDevice, st.stream));
-        h2d_bytes += 4 * avail;
+    st.chunk_words = std::max<int64_t>(1, (avail + kChunks - 1) / kChunks);
+    cudaStream_t cs = streamed ? st.copy : st.stream;
+    SG_CUDA_CHECK(cudaMemsetAsync(st.ready.p, 0, 4 * kChunks, st.stream));
+    if (streamed) {
+        SG_CUDA_CHECK(cudaEventRecord(st.copy_go, st.stream));
+        SG_CUDA_CHECK(cudaStreamWaitEvent(st.copy, st.copy_go, 0));
     }
     if (static_cast<size_t>(4 * avail) < seq_bytes)
         SG_CUDA_CHECK(cudaMemsetAsync(static_cast<char*>(st.seq.p) + 4 * avail, 0,
-                                      seq_bytes - 4 * static_cast<size_t>(avail), st.stream));
+                                      seq_bytes - 4 * static_cast<size_t>(avail), cs));
+    for (int c = 0; c < kChunks; ++c) {
+        const int64_t lo = std::min<int64_t>(avail, c * st.chunk_words);
+        const int64_t hi = std::min<int64_t>(avail, lo + st.chunk_words);
+        if (hi > lo) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.as<uint32_t>() + lo, in->seq + pp.word_lo + lo,
+                                          4 * static_cast<size_t>(hi - lo), cudaMemcpyHostToDevice, cs));
+            h2d_bytes += 4 * (hi - lo);
+        }
+        SG_CUDA_CHECK(cudaMemsetAsync(st.ready.as<uint32_t>() + c, 1, 4, cs));
+    }
     if (pp.any_n) {
         const int64_t mlo = pp.word_lo / 2;
         const int64_t mwords = (words + 1) / 2 + 4;
@@ -614,6 +657,9 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.scratch = st.scratch.as<uint32_t>();
     p.bnd = st.bnd.as<uint32_t>();
     p.next_pair = st.next_pair.as<unsigned int>();
+    p.ready = st.ready.as<unsigned int>();
+    p.chunk_words = st.chunk_words;
+    p.n_chunks = kChunks;
     p.phase_cycles = nullptr;
     p.warp_times = nullptr;
     if (const char* e = getenv("SG_WARP_TIMES")) {  // diagnostics
@@ -816,10 +862,23 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             DevState& st = *slot.st;
             states[d] = &st;
             const Shard s{in, cut[d], cut[d + 1]};
+            const bool trace = getenv("SG_TRACE") != nullptr;  // development aid
+            auto mark = [&](const char* what) {
+                if (!trace) return;
+                cudaStreamSynchronize(st.stream);
+                std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", what,
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
+            };
+            mark("start");
             prep_shard(s, prep[d], mixed);
-            o.h2d_bytes = upload_shard(st, s, prep[d]);
+            mark("prep");
+            o.h2d_bytes = upload_shard(st, s, prep[d], /*streamed=*/!getenv("SG_NO_STREAM"));
+            mark("upload");
             o.launches = launch_shard(st, rcfg, prep[d]);
+            mark("kernels");
             fetch_small(st, prep[d].n, o);
+            mark("fetch");
         } catch (const Fail& f) {
             o.err = f.code;
             o.msg = g_last_error;
@@ -857,6 +916,10 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             }
             scatter_small(out, cut[d], cut[d + 1] - cut[d], run_base[d], o);
             SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+            if (getenv("SG_TRACE"))
+                std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "runs+scat",
+                             std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now() - t0).count());
         } catch (const Fail& f) {
             o.err = f.code;
             o.msg = g_last_error;

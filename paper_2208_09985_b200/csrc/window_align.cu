@@ -737,6 +737,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         m_tot = P.pat_len[pair];
         tbase = P.text_off[pair];
         pbase = P.pat_off[pair];
+        {   // streamed upload: wait until the pair's sequence words have arrived
+            const int64_t lw = (max(tbase + n_tot, pbase + m_tot) + 15) >> 4;
+            const int64_t cw = lw / P.chunk_words;
+            const int c = cw < P.n_chunks - 1 ? static_cast<int>(cw) : P.n_chunks - 1;
+            while (*reinterpret_cast<const volatile unsigned*>(P.ready + c) == 0u) __nanosleep(1000);
+        }
         hasn = P.has_n ? P.has_n[pair] != 0 : false;
         toff = poff = 0;
         dist = nwin = status = 0;

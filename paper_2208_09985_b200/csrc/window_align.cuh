@@ -67,6 +67,9 @@ struct AlignParams {
     uint32_t* scratch;        // run bytes, (op << 6) | (len - 1)
     uint32_t* bnd;            // parked rows: per warp [32L + 1 columns][32 lanes][L]
     unsigned int* next_pair;  // work queue head
+    const unsigned int* ready;  // [n_chunks] sequence-word chunk has arrived (streamed upload)
+    int64_t chunk_words;
+    int32_t n_chunks;
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
