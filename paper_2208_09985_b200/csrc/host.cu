@@ -433,7 +433,7 @@ bool any_bits(const uint32_t* m, int64_t base, int64_t len) {
     return false;
 }
 
-void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first) {
+void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split = 0) {
     const sg_packed_pairs* in = s.in;
     const int64_t n = s.hi - s.lo;
     pp.n = n;
@@ -479,27 +479,35 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first) {
     if (pp.ordered) {
         pp.order.ensure(4 * static_cast<size_t>(n));
         int32_t* o = pp.order.as<int32_t>();
-        // longest first, ties in input order: a stable LSD radix sort on the
-        // complemented length key (two 16-bit digits), O(n)
-        std::vector<uint32_t> key(static_cast<size_t>(n)), k2(static_cast<size_t>(n));
-        std::vector<int32_t> tmp(static_cast<size_t>(n));
-        for (int64_t k = 0; k < n; ++k) {
-            o[k] = static_cast<int32_t>(k);
-            key[k] = ~static_cast<uint32_t>(
-                std::min<int64_t>(in->text_len[s.lo + k] + in->pat_len[s.lo + k], 0xFFFFFFFFll));
-        }
-        for (int shift = 0; shift < 32; shift += 16) {
-            std::vector<int64_t> cnt(65537, 0);
-            for (int64_t k = 0; k < n; ++k) ++cnt[((key[k] >> shift) & 0xFFFF) + 1];
-            for (int b = 0; b < 65536; ++b) cnt[b + 1] += cnt[b];
-            for (int64_t k = 0; k < n; ++k) {
-                const int64_t dst = cnt[(key[k] >> shift) & 0xFFFF]++;
-                tmp[dst] = o[k];
-                k2[dst] = key[k];
+        // Longest first, ties in input order (a stable LSD radix sort on the
+        // complemented length key, two 16-bit digits, O(n)). With a split, the
+        // pairs before it (the first round of lanes, the first sequence words to
+        // arrive in a streamed upload) are ordered among themselves, then the rest.
+        auto lpt = [&](int64_t lo, int64_t hi) {
+            const int64_t m = hi - lo;
+            std::vector<uint32_t> key(static_cast<size_t>(m)), k2(static_cast<size_t>(m));
+            std::vector<int32_t> tmp(static_cast<size_t>(m));
+            for (int64_t k = 0; k < m; ++k) {
+                o[lo + k] = static_cast<int32_t>(lo + k);
+                key[k] = ~static_cast<uint32_t>(std::min<int64_t>(
+                    in->text_len[s.lo + lo + k] + in->pat_len[s.lo + lo + k], 0xFFFFFFFFll));
             }
-            std::copy(tmp.begin(), tmp.end(), o);
-            key.swap(k2);
-        }
+            for (int shift = 0; shift < 32; shift += 16) {
+                std::vector<int64_t> cnt(65537, 0);
+                for (int64_t k = 0; k < m; ++k) ++cnt[((key[k] >> shift) & 0xFFFF) + 1];
+                for (int b = 0; b < 65536; ++b) cnt[b + 1] += cnt[b];
+                for (int64_t k = 0; k < m; ++k) {
+                    const int64_t dst = cnt[(key[k] >> shift) & 0xFFFF]++;
+                    tmp[dst] = o[lo + k];
+                    k2[dst] = key[k];
+                }
+                std::copy(tmp.begin(), tmp.end(), o + lo);
+                key.swap(k2);
+            }
+        };
+        const int64_t cut = split > 0 && split < n ? split : n;
+        lpt(0, cut);
+        if (cut < n) lpt(cut, n);
     }
 }
 
@@ -534,7 +542,7 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
 // go on the copy stream, each followed by its ready flag, while K1 already runs
 // on the main stream; a lane waits for the piece holding its pair's last word
 // (K1 fetch). Otherwise (sessions) everything is copied and flagged up front.
-constexpr int kChunks = 8;
+constexpr int kChunks = 16;
 
 int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool streamed = false) {
     const int64_t n = pp.n;
@@ -598,6 +606,23 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool str
 }
 
 // Sizes the per-run buffers and launches K1, K2 (3 kernels) and K3.
+// K1 grid for n pairs. Each lane aligns whole pairs one after another, so a
+// batch takes about ceil(n / lanes) pair-times. Use the fewest lanes that keep
+// that number of rounds (fewer warps per SM run each round faster).
+long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
+    int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    const int wpb = sgk::k1_warps_per_block(rc.L);
+    const long long max_grid = static_cast<long long>(st.sms) * blocks_per_sm;
+    const long long max_lanes = max_grid * wpb * 32;
+    const long long rounds = std::max(1LL, (static_cast<long long>(n) + max_lanes - 1) / max_lanes);
+    const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
+    long long grid = (lanes_needed + 32LL * wpb - 1) / (32LL * wpb);
+    if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
+    if (const char* e = getenv("SG_BLOCKS")) grid = std::max(1LL, std::min(atoll(e), max_grid));
+    return std::max(1LL, std::min(grid, max_grid));
+}
+
 // Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
 int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     const int64_t n = pp.n;
@@ -612,20 +637,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     st.dense_off.ensure(8 * (n1 + 1));
     st.dense.ensure(static_cast<size_t>(pp.scratch_bytes));
     st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
-    int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
     const int wpb = sgk::k1_warps_per_block(rc.L);
-    // Each lane aligns whole pairs one after another, so a batch takes about
-    // ceil(n / lanes) pair-times. Use the fewest lanes that keep that number of
-    // rounds (fewer warps per SM run each round faster).
-    const long long max_grid = static_cast<long long>(st.sms) * blocks_per_sm;
-    const long long max_lanes = max_grid * wpb * 32;
-    const long long rounds = std::max(1LL, (static_cast<long long>(n) + max_lanes - 1) / max_lanes);
-    const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
-    long long grid = (lanes_needed + 32LL * wpb - 1) / (32LL * wpb);
-    if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
-    if (const char* e = getenv("SG_BLOCKS")) grid = std::max(1LL, std::min(atoll(e), max_grid));
-    grid = std::max(1LL, std::min(grid, max_grid));
+    const long long grid = k1_grid(st, rc, n);
     st.grid = grid;
     st.lanes = grid * wpb * 32;
     st.bnd.ensure(sgk::bnd_scratch_bytes(rc.L, grid * wpb));
@@ -871,9 +884,14 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
                                  std::chrono::steady_clock::now() - t0).count());
             };
             mark("start");
-            prep_shard(s, prep[d], mixed);
+            // streamed: the first round of lanes takes pairs from the front of memory
+            const bool streamed = !getenv("SG_NO_STREAM");
+            const int64_t split = streamed ? k1_grid(st, rcfg, s.hi - s.lo) *
+                                                 sgk::k1_warps_per_block(rcfg.L) * 32
+                                           : 0;
+            prep_shard(s, prep[d], mixed, split);
             mark("prep");
-            o.h2d_bytes = upload_shard(st, s, prep[d], /*streamed=*/!getenv("SG_NO_STREAM"));
+            o.h2d_bytes = upload_shard(st, s, prep[d], streamed);
             mark("upload");
             o.launches = launch_shard(st, rcfg, prep[d]);
             mark("kernels");

@@ -102,21 +102,6 @@ __device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t two, uint32_t 
     return r;
 }
 
-// NW words of 2-bit codes starting at base `base` (base k at bits 2(k%16)).
-template <int NW>
-__device__ __forceinline__ void load_codes(const uint32_t* __restrict__ seq, int64_t base,
-                                           uint32_t (&w)[NW]) {
-    const uint32_t* src = seq + (base >> 4);
-    const int s = static_cast<int>(base & 15) * 2;
-    uint32_t prev = __ldg(src);
-#pragma unroll
-    for (int k = 0; k < NW; ++k) {
-        const uint32_t nx = __ldg(src + k + 1);
-        w[k] = __funnelshift_r(prev, nx, s);
-        prev = nx;
-    }
-}
-
 // NW words of a 1-bit-per-base mask starting at base `base`.
 template <int NW>
 __device__ __forceinline__ void load_bits(const uint32_t* __restrict__ mask, int64_t base,
@@ -592,6 +577,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
     // Pattern masks, text codes and packed sequences of the current segment.
     auto load_segment = [&]() {
         const int off = WB - m_w;
+        // Sequence words load through L2 only (ld.global.cg): with a streamed
+        // upload a line read early into L1 could hold words of a chunk that had
+        // not arrived yet (the staging reads run past the pair's end).
         uint32_t pw[NW + 1], pn[L + 1], tw[NW + 1], tn[L + 1];
         {
             const int64_t ta = tbase + toff, pa = pbase + poff;
@@ -602,12 +590,12 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             if (!hit_t) {
                 nx_tw = wt;
 #pragma unroll
-                for (int k = 0; k < PFW; ++k) nx_t[k] = __ldg(P.seq + wt + k);
+                for (int k = 0; k < PFW; ++k) nx_t[k] = __ldcg(P.seq + wt + k);
             }
             if (!hit_p) {
                 nx_pw = wp;
 #pragma unroll
-                for (int k = 0; k < PFW; ++k) nx_p[k] = __ldg(P.seq + wp + k);
+                for (int k = 0; k < PFW; ++k) nx_p[k] = __ldcg(P.seq + wp + k);
             }
 #pragma unroll
             for (int k = 0; k < PFW; ++k) {
@@ -629,8 +617,8 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             nx_pw = wp;
 #pragma unroll
             for (int k = 0; k < PFW; ++k) {
-                nx_t[k] = __ldg(P.seq + wt + k);
-                nx_p[k] = __ldg(P.seq + wp + k);
+                nx_t[k] = __ldcg(P.seq + wt + k);
+                nx_p[k] = __ldcg(P.seq + wp + k);
             }
         }
 #pragma unroll
