@@ -186,6 +186,29 @@ int sg_synth_packed(int cfg_id, int64_t first, int64_t count, sg_packed_pairs* o
 int sg_synth_codes(int cfg_id, int64_t first, int64_t count, sg_pairs* out);
 void sg_pairs_free(sg_pairs* p);
 
+/* ---- pair files and result output (the CLI's data path) ----------------
+ * sg_read_pairs reads the reference's pair formats straight into packed form:
+ *   SG_FORMAT_TSV        `id<TAB>text<TAB>pattern` per line (read_pairs_tsv,
+ *                        proj/src/io.cpp:66-94);
+ *   SG_FORMAT_FASTA_PAIR "<text.fa>,<pattern.fa>", records paired in order
+ *                        (read_pairs_fasta, io.cpp:96-112; read_pairs io.cpp:114-121).
+ * Sequences are upper-cased; CR line ends and empty lines are skipped; ids
+ * must be unique. Errors are SG_INPUT with the reference's messages.
+ * sg_write_results writes `id<TAB>distance<TAB>cigar` lines, "*" for a pair
+ * that was not found (write_batch_tsv, proj/src/batch.cpp:106-113), or with
+ * json != 0 the CLI's JSON array (proj/tools/main.cpp:77-88). path NULL or
+ * "-" writes to stdout. */
+enum { SG_FORMAT_TSV = 0, SG_FORMAT_FASTA_PAIR = 1 };
+typedef struct sg_pair_file {
+    int64_t n_pairs;
+    const char* const* ids;  /* [n_pairs] NUL-terminated */
+    sg_packed_pairs packed;  /* owned; pass to sg_align_packed */
+    void* _owner;
+} sg_pair_file;
+int sg_read_pairs(const char* input, int format, sg_pair_file* out);
+void sg_pair_file_free(sg_pair_file* f);
+int sg_write_results(const char* path, const sg_pair_file* pairs, const sg_results* res, int json);
+
 #ifdef __cplusplus
 }
 #endif

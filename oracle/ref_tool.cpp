@@ -10,10 +10,13 @@
 //   ref_tool align  --input pairs.tsv [cfg flags] [--hash]   per-pair results
 //   ref_tool synth  --cfg N --first F --count C [cfg flags] [--hash]
 //   ref_tool bench  --cfg N --first F --count C --threads T [cfg flags]
+//   ref_tool read --input pairs.tsv | read-fasta --input a.fa,b.fa   parsed pairs
+//   ref_tool cli-tsv --input pairs.tsv [cfg flags]   write_batch_tsv output
 // cfg flags: --W w --O o --sene 0|1 --dent 0|1 --et 0|1 --mode windowed|single --k k
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <iostream>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -125,6 +128,16 @@ int main(int argc, char** argv) {
         if (a.cmd == "align") {
             const auto pairs = scrooge::read_pairs_tsv(a.input);
             print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);
+        } else if (a.cmd == "read" || a.cmd == "read-fasta") {
+            // the reference readers (io.cpp:66-121): parsed pairs, or the error
+            const auto pairs = scrooge::read_pairs(
+                a.input, a.cmd == "read" ? scrooge::PairFormat::Tsv : scrooge::PairFormat::FastaPair);
+            for (const auto& p : pairs)
+                std::printf("%s\t%s\t%s\n", p.id.c_str(), p.text.c_str(), p.pattern.c_str());
+        } else if (a.cmd == "cli-tsv") {
+            // run_align's TSV output path (main.cpp:152-167): read_pairs, run_batch, write_batch_tsv
+            const auto pairs = scrooge::read_pairs(a.input, scrooge::PairFormat::Tsv);
+            scrooge::write_batch_tsv(std::cout, pairs, scrooge::run_batch(pairs, a.config, a.threads));
         } else if (a.cmd == "synth") {
             const auto pairs = synth_pairs(a);
             print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);

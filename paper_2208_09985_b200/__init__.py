@@ -9,6 +9,7 @@ from .aligner import (  # noqa: F401
     InputError, InstrumentationCounters, InternalError, OutOfStoredRegionError, PackedBatch,
     PairOutcome, Results, SeqPairRecord, Session, align, align_codes, align_packed,
     cigar_from_string, cigar_to_string, decode_sequence, encode_sequence, last_transfer_bytes,
-    pack, run_batch, synth_codes, synth_packed, write_batch_tsv,
+    pack, run_batch, synth_codes, synth_packed, write_batch_tsv, PairFile, read_pairs,
+    write_results,
 )
 from .build import LIB as LIBRARY_PATH  # noqa: F401

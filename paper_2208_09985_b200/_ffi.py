@@ -23,7 +23,7 @@ EXPORTS = (
     "sg_cigar_string", "sg_cigar_runs", "sg_pack", "sg_packed_free",
     "sg_last_transfer_bytes", "sg_session_create", "sg_session_run", "sg_session_fetch",
     "sg_session_info", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
-    "sg_pairs_free", "sg_alu_peak",
+    "sg_pairs_free", "sg_alu_peak", "sg_read_pairs", "sg_pair_file_free", "sg_write_results",
 )
 
 
@@ -43,6 +43,11 @@ class SgPackedPairs(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("seq", C.c_void_p), ("seq_words", C.c_int64),
                 ("nmask", C.c_void_p), ("text_off", C.c_void_p), ("text_len", C.c_void_p),
                 ("pat_off", C.c_void_p), ("pat_len", C.c_void_p)]
+
+
+class SgPairFile(C.Structure):
+    _fields_ = [("n_pairs", C.c_int64), ("ids", C.POINTER(C.c_char_p)),
+                ("packed", SgPackedPairs), ("_owner", C.c_void_p)]
 
 
 class SgResults(C.Structure):
@@ -103,6 +108,10 @@ def load(build_if_missing: bool = True):
     L.sg_pairs_free.argtypes = [P(SgPairs)]
     L.sg_pairs_free.restype = None
     L.sg_alu_peak.argtypes = [C.c_int, P(C.c_double), P(C.c_double), P(C.c_double)]
+    L.sg_read_pairs.argtypes = [C.c_char_p, C.c_int, P(SgPairFile)]
+    L.sg_pair_file_free.argtypes = [P(SgPairFile)]
+    L.sg_pair_file_free.restype = None
+    L.sg_write_results.argtypes = [C.c_char_p, P(SgPairFile), P(SgResults), C.c_int]
     _lib = L
     return L
 

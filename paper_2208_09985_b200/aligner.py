@@ -371,6 +371,69 @@ def pack(batch: CodesBatch) -> PackedBatch:
     return PackedBatch(out)
 
 
+class PairFile:
+    """Pairs read from a TSV or FASTA-pair file (sg_read_pairs; io.cpp:66-121),
+    already 2-bit packed. `.packed` goes to align_packed; `.ids` are the pair ids."""
+
+    def __init__(self, f: _ffi.SgPairFile):
+        self._f = f
+        self.n = int(f.n_pairs)
+        self.ids = [f.ids[k].decode() for k in range(self.n)]
+        self.packed = _PackedView(f.packed, self)
+
+    def codes(self, k: int):
+        """(text, pattern) of pair k as 1-byte codes (0..3 ACGT, 4 other)."""
+        return _unpack(self._f.packed, k)
+
+    def __del__(self):
+        try:
+            _ffi.load().sg_pair_file_free(C.byref(self._f))
+        except Exception:
+            pass
+
+
+class _PackedView:
+    """Non-owning view of packed pairs held by another object."""
+
+    def __init__(self, p: _ffi.SgPackedPairs, owner):
+        self._p, self._owner, self.n = p, owner, p.n_pairs
+
+    @property
+    def c(self) -> _ffi.SgPackedPairs:
+        return self._p
+
+
+def _unpack(p: _ffi.SgPackedPairs, k: int):
+    def one(off_ptr, len_ptr):
+        off = C.cast(off_ptr, C.POINTER(C.c_int64))[k]
+        n = C.cast(len_ptr, C.POINTER(C.c_int64))[k]
+        idx = np.arange(off, off + n, dtype=np.int64)
+        words = np.ctypeslib.as_array(C.cast(p.seq, C.POINTER(C.c_uint32)), (int(p.seq_words),))
+        codes = ((words[idx >> 4] >> (2 * (idx & 15)).astype(np.uint32)) & 3).astype(np.uint8)
+        if p.nmask:
+            nw = (int(p.seq_words) * 16 + 31) // 32
+            nm = np.ctypeslib.as_array(C.cast(p.nmask, C.POINTER(C.c_uint32)), (nw,))
+            codes[((nm[idx >> 5] >> (idx & 31).astype(np.uint32)) & 1) == 1] = 4
+        return codes.tobytes()
+    return one(p.text_off, p.text_len), one(p.pat_off, p.pat_len)
+
+
+def read_pairs(path: str, fmt: str = "tsv") -> PairFile:
+    """read_pairs (proj/src/io.cpp:114-121): fmt "tsv" or "fasta-pair"
+    (path = "<text.fa>,<pattern.fa>")."""
+    if fmt not in ("tsv", "fasta-pair"):
+        raise InputError(f"unknown input format '{fmt}' (expected tsv or fasta-pair)")
+    out = _ffi.SgPairFile()
+    _check(_ffi.load().sg_read_pairs(path.encode(), 0 if fmt == "tsv" else 1, C.byref(out)))
+    return PairFile(out)
+
+
+def write_results(path: Optional[str], pairs: PairFile, res: "Results", json: bool = False) -> None:
+    """write_batch_tsv (batch.cpp:106-113) or the CLI's JSON (main.cpp:77-88)."""
+    _check(_ffi.load().sg_write_results(path.encode() if path else None, C.byref(pairs._f),
+                                        C.byref(res._res), int(bool(json))))
+
+
 def synth_packed(cfg_id: int, first: int = 0, count: int = -1) -> PackedBatch:
     """BASELINE config `cfg_id` pairs [first, first+count), 2-bit packed (csrc/synth.h)."""
     out = _ffi.SgPackedPairs()

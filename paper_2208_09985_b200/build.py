@@ -13,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libscrooge_b200.so")
-SOURCES = ["window_align.cu", "host.cu", "peak.cu", "synth.c"]
+SOURCES = ["window_align.cu", "host.cu", "peak.cu", "synth.c", "io.cpp"]
+CLI = os.path.join(LIB_DIR, "sg_align")  # the align / bench CLI (csrc/sg_align.cpp)
 HEADERS = ["window_align.cuh", "synth.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -36,7 +37,8 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "scrooge_b200.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+    deps.append(os.path.join(CSRC, "sg_align.cpp"))
+    return not os.path.exists(CLI) or any(os.path.getmtime(d) > t for d in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -52,6 +54,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode})")
     with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as f:
         f.write(res.stderr)
+    cli = subprocess.run(["g++", "-O2", "-std=c++17", "-o", CLI, os.path.join(CSRC, "sg_align.cpp"),
+                          "-L" + LIB_DIR, "-lscrooge_b200", "-Wl,-rpath,$ORIGIN"],
+                         capture_output=True, text=True)
+    if cli.returncode:
+        sys.stderr.write(cli.stdout + cli.stderr)
+        raise RuntimeError("g++ failed building sg_align")
     return LIB
 
 

@@ -36,6 +36,17 @@ int set_error(int code, const char* fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+namespace sgk {
+int set_error_msg(int code, const std::string& msg) {  // for io.cpp
+    g_last_error = msg;
+    return code;
+}
+}  // namespace sgk
+
+namespace {
+
 struct Fail {  // thrown inside the runtime, converted to a status at the ABI
     int code;
 };
