@@ -190,6 +190,7 @@ struct DevState {
     DevBuf seq, nmask, text_off, pat_off, text_len, pat_len, has_n, order;
     DevBuf distance, windows, status, out_bytes, counters, bound_off, scratch, bnd, next_pair;
     DevBuf ready;                    // per-chunk "sequence words arrived" flags (streamed upload)
+    DevBuf bnd_ones, bnd_zeros;      // constant parked rows (one warp's slots, L = 4 size)
     cudaStream_t copy = nullptr;     // H2D of the sequence words, overlapping K1
     cudaEvent_t copy_go = nullptr;
     int64_t chunk_words = 1;
@@ -210,7 +211,8 @@ struct DevState {
         cudaSetDevice(device);
         for (DevBuf* b : {&seq, &nmask, &text_off, &pat_off, &text_len, &pat_len, &has_n, &order,
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
-                          &scratch, &bnd, &next_pair, &ready, &dense_off, &dense, &scan_tmp})
+                          &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
+                          &dense, &scan_tmp})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
@@ -653,6 +655,13 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     st.grid = grid;
     st.lanes = grid * wpb * 32;
     st.bnd.ensure(sgk::bnd_scratch_bytes(rc.L, grid * wpb));
+    if (!st.bnd_ones.p) {
+        const size_t cb = sgk::bnd_scratch_bytes(4, 1);
+        st.bnd_ones.ensure(cb);
+        st.bnd_zeros.ensure(cb);
+        SG_CUDA_CHECK(cudaMemsetAsync(st.bnd_ones.p, 0xFF, cb, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.bnd_zeros.p, 0, cb, st.stream));
+    }
     SG_CUDA_CHECK(cudaMemsetAsync(st.next_pair.p, 0, 4, st.stream));
 
     sgk::AlignParams p{};
@@ -680,6 +689,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.bound_off = st.bound_off.as<int64_t>();
     p.scratch = st.scratch.as<uint32_t>();
     p.bnd = st.bnd.as<uint32_t>();
+    p.bnd_ones = st.bnd_ones.as<uint32_t>();
+    p.bnd_zeros = st.bnd_zeros.as<uint32_t>();
     p.next_pair = st.next_pair.as<unsigned int>();
     p.ready = st.ready.as<unsigned int>();
     p.chunk_words = st.chunk_words;

@@ -94,6 +94,13 @@ __device__ __forceinline__ uint32_t lds_v(const uint32_t* p) {
     return v;
 }
 
+// A value the compiler cannot see through (keeps x * (1 << P) an IMAD).
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+    uint32_t r;
+    asm("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
 // x*two + b with `two` a runtime 2: an IMAD on the FMA pipe. With a literal 2
 // ptxas emits LEA, which issues on the ALU pipe the bitvector logic needs.
 __device__ __forceinline__ uint32_t dp_shift(uint32_t x, uint32_t two, uint32_t b) {
@@ -312,6 +319,8 @@ __device__ __forceinline__ uint32_t top_bit(const Sweep<L, R>& S, int r, int r0,
 template <int L>
 struct LaneMem {
     uint32_t* bnd;        // + lane * L
+    const uint32_t* ones;   // + lane * L: all-ones rows (R[.][-1], a window's first chunk)
+    const uint32_t* zeros;  // + lane * L: all-zero rows (idle lanes)
     uint32_t* xy;         // + lane * 2
     const uint32_t* pm;   // + lane * L
     const uint32_t* txt;  // + lane
@@ -346,13 +355,14 @@ template <int L, int R, int C, int MODE, bool DRAIN>
 __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const LaneMem<L>& M,
                                             uint32_t codes4, uint32_t codes4n, int col_top,
                                             uint32_t two, uint32_t one, int g0, bool z0, int n_w,
-                                            uint32_t keep_old, uint32_t lv, int r0, int p0,
-                                            int off, int& fr) {
+                                            const uint32_t* rb, int r0, int p0, int off, int& fr) {
     static_assert(R == 4, "groups are aligned to 4-column text-code words");
     constexpr int WB = 32 * L;
     constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
-    // group bases: row-0 parked-row slot of step 0, finished column of step 0
-    const uint32_t* nbg = M.bnd + (col_top + 4) * 32 * L;
+    // group bases: row-0 parked-row slot of step 0 (read from rb: the parked
+    // row, or all ones in a window's first chunk, or zeros for an idle lane),
+    // finished column of step 0
+    const uint32_t* nbg = rb + (col_top + 4) * 32 * L;
     const int colf0 = col_top + R - 1;
     uint32_t* pbg = M.bnd + (colf0 + 4) * 32 * L;
     uint32_t* pxg = M.xy + colf0 * 64;
@@ -362,7 +372,7 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
                                                                : pxg);
         F.ox = o.x;
         F.oy = o.y;
-        mul = 1u << band_base<L>(colf0, off);
+        mul = opaque_u32(1u << band_base<L>(colf0, off));  // keeps band_word's x * 2^P an IMAD
     }
 #define SG_STEP(U)                                                                           \
     if (!DRAIN || (U) + 1 < R) {                                                             \
@@ -370,10 +380,10 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
         uint32_t pm0[L], north0[L];                                                          \
         _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
             pm0[l] = F.pmn[l];                                                               \
-            north0[l] = (F.nbr[(U)][l] | ~keep_old) & lv; /* first chunk: R[.][-1] = ones */\
+            north0[l] = F.nbr[(U)][l];                                                       \
         }                                                                                    \
         {   /* prefetch: parked row one group ahead, pattern mask of the next column */     \
-            const uint32_t* src = DRAIN ? M.bnd : nbg - ((U) + 4) * 32 * L;                  \
+            const uint32_t* src = DRAIN ? rb : nbg - ((U) + 4) * 32 * L;                     \
             _Pragma("unroll") for (int l = 0; l < L; ++l) F.nbr[(U)][l] = src[l];            \
             const uint32_t w = (U) == 3 ? codes4n : codes4;                                  \
             const int code = static_cast<int>((w >> (8 * ((2 - (U)) & 3))) & 0xFFu);         \
@@ -392,8 +402,8 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
             _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];             \
             if (CAP) {                                                                       \
                 uint2 o;                                                                     \
-                o.x = (F.ox & keep_old) | band_word<L>(S.acc[SL][0], mul);                   \
-                o.y = (F.oy & keep_old) | band_word<L>(S.acc[SL][1], mul);                   \
+                o.x = F.ox | band_word<L>(S.acc[SL][0], mul); /* cleared per window */      \
+                o.y = F.oy | band_word<L>(S.acc[SL][1], mul);                                \
                 *reinterpret_cast<uint2*>(px) = o;                                           \
                 if ((U) + 1 < R) { /* next step's column; groups reload at their start */   \
                     const uint2 n = *reinterpret_cast<const uint2*>(                         \
@@ -436,7 +446,7 @@ __device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int
     const int tsteps = ((n_max + R - 1) / R) * R;
     const int S0 = tsteps - 1;
     const bool z0 = d0 == 0 && live;
-    const uint32_t keep_old = d0 > 0 || !live ? ~0u : 0u;
+    const uint32_t* rb = !live ? M.zeros : (d0 == 0 ? M.ones : M.bnd);
     // Virtual columns >= n_w of the parked row hold R[n][d0-1].
     if (d0 > 0)
         for (int c = n_w; c <= S0; ++c)
@@ -446,7 +456,7 @@ __device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int l = 0; l < L; ++l) F.nbr[u][l] = M.bnd[(S0 - u + 4) * 32 * L + l];
+        for (int l = 0; l < L; ++l) F.nbr[u][l] = rb[(S0 - u + 4) * 32 * L + l];
     uint32_t codes4 = M.txt[((S0 >> 2) + 1) * 32];
     {
         const int code = static_cast<int>((codes4 >> 24) & 0xFFu);  // column S0 = 3 mod 4
@@ -467,19 +477,19 @@ __device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int
         }
         if (mode == kIn)
             sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
-                                             n_w, keep_old, lv, r0, p0, off, fr);
+                                             n_w, rb, r0, p0, off, fr);
         else if (mode == kOut)
             sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                              z0, n_w, keep_old, lv, r0, p0, off, fr);
+                                              z0, n_w, rb, r0, p0, off, fr);
         else
             sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                               z0, n_w, keep_old, lv, r0, p0, off, fr);
+                                               z0, n_w, rb, r0, p0, off, fr);
         codes4 = codes4n;
     }
     // drain: rows 1..R-1 finish (row 0 has just left column 0)
     if (!top_bit<L, R>(S, 0, r0, p0)) fr = 0;
     sweep_group<L, R, C, kSlow, true>(S, F, M, codes4, codes4, -1, two, one,
-                                      n_w - S0 - d0 + tsteps, z0, n_w, keep_old, lv, r0, p0, off, fr);
+                                      n_w - S0 - d0 + tsteps, z0, n_w, rb, r0, p0, off, fr);
     return fr;
 }
 
@@ -505,7 +515,8 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
     const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
     uint32_t* const bnd = P.bnd + gwarp * (WB + 5) * 32 * L;    // [WB+5][32][L]
     const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
-    const LaneMem<L> lmem{bnd + lane * L, xy + lane * 2, pmv + lane * L,
+    const LaneMem<L> lmem{bnd + lane * L, P.bnd_ones + lane * L, P.bnd_zeros + lane * L,
+                          xy + lane * 2, pmv + lane * L,
                           reinterpret_cast<const uint32_t*>(txt) + lane};
 
 #pragma unroll
@@ -660,6 +671,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                                                           | (0x04040404u << (8 * valid));
             txt32[(h + 1) * 32 + lane] = c;
         }
+        // the segment's traceback events start empty (chunks OR into them)
+#pragma unroll 4
+        for (int c = 0; c <= C; ++c) *reinterpret_cast<uint2*>(xy + c * 64 + lane * 2) = make_uint2(0u, 0u);
         // N words of the segment for the traceback's match runs
 #pragma unroll
         for (int k = 0; k <= L; ++k) {

@@ -65,7 +65,9 @@ struct AlignParams {
     uint64_t* counters;       // [n_pairs][7] (InstrumentationCounters order) or null
     const int64_t* bound_off; // byte offset (4-aligned) of each pair's run region in scratch
     uint32_t* scratch;        // run bytes, (op << 6) | (len - 1)
-    uint32_t* bnd;            // parked rows: per warp [32L + 1 columns][32 lanes][L]
+    uint32_t* bnd;            // parked rows: per warp [32L + 5 slots][32 lanes][L]
+    const uint32_t* bnd_ones;   // one warp's worth of parked-row slots holding ones / zeros,
+    const uint32_t* bnd_zeros;  // read in a window's first chunk / by an idle lane
     unsigned int* next_pair;  // work queue head
     const unsigned int* ready;  // [n_chunks] sequence-word chunk has arrived (streamed upload)
     int64_t chunk_words;
