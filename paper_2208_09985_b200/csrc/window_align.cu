@@ -881,31 +881,10 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             const int lim = limit >= 0 ? limit : 0x3FFFFFFF;
             unsigned reads = 0;
             ++ph_tbn;
-            // interior: both sides left, inside the stored event columns
-            for (;;) {
-                ++ph_steps;
-                ++tb_trip;
-                const int rem = lim - steps;
-                if (rem == 0 || i == n_w || j == m_w || i >= C) break;
-                // event words of (i, j) and the match-run words load together
-                const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
-                const uint32_t xw = ev.x, yw = ev.y;
-                const unsigned q = static_cast<unsigned>(j + off);
-                const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
-                if (static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
-                const uint32_t bit = 0x80000000u >> ((32 / L) * (q % L) + dp);
-                const int run = match_run(i, j);
-                const bool ed = run == 0;  // the other bounds are >= 1 here
-                const int k = ed ? 1 : min(min(run, rem), min(min(n_w - i, m_w - j), C - i));
-                const int op = ed ? (xw & bit ? 1 : (yw & bit ? 3 : 2)) : 0;
-                if (ed && d == 0) status = kStInternal | kDetNoStep;
-                reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
-                i += op != 2 ? k : 0;
-                j += op != 3 ? k : 0;
-                d -= ed;
-                dist += ed;
-                steps += k;
-                // emit (k <= 16): extend the open byte, or write it and open the next
+            // interior: both sides left, inside the stored event columns. One
+            // trip takes a run of matches and then, where the run stopped at a
+            // mismatch, the edit there (its event words load after the run).
+            auto emit_short = [&](int op, int k) {  // k <= 16: extend the open byte or write it
                 if (op == cur_op && cur_len + k <= 64) {
                     cur_len += k;
                 } else {
@@ -916,6 +895,38 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                     cur_len = same ? cur_len + k - 64 : k;
                     cur_op = op;
                 }
+            };
+            for (;;) {
+                ++ph_steps;
+                ++tb_trip;
+                int rem = lim - steps;
+                if (rem == 0 || i == n_w || j == m_w || i >= C) break;
+                const int run = match_run(i, j);
+                const int k = min(min(run, rem), min(min(n_w - i, m_w - j), C - i));
+                if (k > 0) {
+                    reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
+                    i += k;
+                    j += k;
+                    steps += k;
+                    rem -= k;
+                    emit_short(0, k);
+                }
+                if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w || i >= C) continue;
+                // the edit at the mismatch (i, j)
+                const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
+                const unsigned q = static_cast<unsigned>(j + off);
+                const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
+                if (static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
+                const uint32_t bit = 0x80000000u >> ((32 / L) * (q % L) + dp);
+                const int op = ev.x & bit ? 1 : (ev.y & bit ? 3 : 2);
+                if (d == 0) status = kStInternal | kDetNoStep;
+                reads += d == 0 ? 1u : 3u;
+                i += op != 2;
+                j += op != 3;
+                --d;
+                ++dist;
+                ++steps;
+                emit_short(op, 1);
             }
             // tail: one side consumed (a single run of indels), or the next
             // column has no stored events (continue on the suffix)
