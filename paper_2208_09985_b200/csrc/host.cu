@@ -258,14 +258,10 @@ int validate_cfg(const sg_config* c) {
                          "trimmed table storage cannot back a full single-window traceback");
     if (c->single_window && (c->k_single < 0 || c->k_single > 1024))
         return set_error(SG_CONFIG, "k out of range: %d", c->k_single);
-    // GPU-path limits (SURVEY §8(b) semantic gaps)
-    if (!c->single_window && !limbs_for(c->W))
-        return set_error(SG_CONFIG, "the GPU path supports W <= 128, got W=%d", c->W);
     return SG_OK;
 }
 
 constexpr int64_t kMaxSingle = 1024;     // BitVector::kMaxBits (bitvec.hpp:29)
-constexpr int64_t kMaxSingleGpu = 128;   // longest single window of the GPU path
 
 int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl, const sg_config* c) {
     for (int64_t k = 0; k < n; ++k) {
@@ -280,10 +276,6 @@ int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl, const sg_c
                 return set_error(SG_INPUT,
                                  "pair '%lld': single-window mode requires sequences of at most "
                                  "1024 characters", static_cast<long long>(k));
-            if (tl[k] > kMaxSingleGpu || pl[k] > kMaxSingleGpu)
-                return set_error(SG_CONFIG,
-                                 "pair '%lld': single-window mode on the GPU path supports "
-                                 "sequences of at most 128 characters", static_cast<long long>(k));
         }
     }
     return SG_OK;
@@ -526,6 +518,8 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split
 
 struct RunConfig {
     int L, W, O, et, policy, single, k_single;
+    bool wide;  // K6 (one warp per pair): windows wider than 128 bits
+    int wcap;   // K6: widest window in columns
 };
 
 unsigned long long* g_phase_buf = nullptr;  // diagnostics (SG_PHASE_CYCLES=1)
@@ -539,11 +533,17 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
     r.L = limbs_for(c->W);
     r.single = c->single_window ? 1 : 0;
     r.k_single = c->k_single;
+    r.wcap = c->W;
     if (r.single) {
         int64_t mx = 1;
         for (int64_t k = 0; k < n; ++k) mx = std::max(mx, std::max(tl[k], pl[k]));
         r.L = limbs_for(static_cast<int>(mx));
+        r.wcap = static_cast<int>(mx);
     }
+    // K6 takes what K1's limb counts do not cover; SG_FORCE_WIDE=1 routes every
+    // batch through it (tests cross-check the two kernels)
+    const char* fw = getenv("SG_FORCE_WIDE");
+    r.wide = r.L == 0 || (fw && fw[0] == '1');
     r.W = c->W;
     r.O = c->O;
     r.et = c->early_termination ? 1 : 0;
@@ -623,6 +623,15 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool str
 // batch takes about ceil(n / lanes) pair-times. Use the fewest lanes that keep
 // that number of rounds (fewer warps per SM run each round faster).
 long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
+    if (rc.wide) {  // K6: one warp per pair, persistent
+        const int wpb = sgk::wide_warps_per_block();
+        const long long bps = std::max(1, sgk::wide_max_blocks_per_sm());
+        long long warps = std::min<long long>(std::max<int64_t>(n, 1), st.sms * bps * wpb);
+        // parked row + events: keep the scratch within 4 GiB
+        const long long per = sgk::wide_warp_words(rc.wcap) * 4;
+        warps = std::max(1LL, std::min(warps, (4LL << 30) / per));
+        return (warps + wpb - 1) / wpb;
+    }
     int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     const int wpb = sgk::k1_warps_per_block(rc.L);
@@ -634,6 +643,12 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
     if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
     if (const char* e = getenv("SG_BLOCKS")) grid = std::max(1LL, std::min(atoll(e), max_grid));
     return std::max(1LL, std::min(grid, max_grid));
+}
+
+// Pairs K1 / K6 work on at once (lanes / warps of the grid).
+int64_t pairs_in_flight(const DevState& st, const RunConfig& rc, int64_t n) {
+    const long long g = k1_grid(st, rc, n);
+    return rc.wide ? g * sgk::wide_warps_per_block() : g * sgk::k1_warps_per_block(rc.L) * 32;
 }
 
 // Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
@@ -650,11 +665,12 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     st.dense_off.ensure(8 * (n1 + 1));
     st.dense.ensure(static_cast<size_t>(pp.scratch_bytes));
     st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
-    const int wpb = sgk::k1_warps_per_block(rc.L);
+    const int wpb = rc.wide ? sgk::wide_warps_per_block() : sgk::k1_warps_per_block(rc.L);
     const long long grid = k1_grid(st, rc, n);
     st.grid = grid;
-    st.lanes = grid * wpb * 32;
-    st.bnd.ensure(sgk::bnd_scratch_bytes(rc.L, grid * wpb));
+    st.lanes = grid * wpb * (rc.wide ? 1 : 32);  // pairs in flight
+    st.bnd.ensure(rc.wide ? static_cast<size_t>(sgk::wide_warp_words(rc.wcap)) * 4 * grid * wpb
+                          : sgk::bnd_scratch_bytes(rc.L, grid * wpb));
     if (!st.bnd_ones.p) {
         const size_t cb = sgk::bnd_scratch_bytes(4, 1);
         st.bnd_ones.ensure(cb);
@@ -695,6 +711,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.ready = st.ready.as<unsigned int>();
     p.chunk_words = st.chunk_words;
     p.n_chunks = kChunks;
+    p.wcap = rc.wcap;
     p.phase_cycles = nullptr;
     p.warp_times = nullptr;
     if (const char* e = getenv("SG_WARP_TIMES")) {  // diagnostics
@@ -721,7 +738,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
     if (n > 0) {
         SG_CUDA_CHECK(static_cast<cudaError_t>(
-            sgk::launch_window_align(rc.L, p, static_cast<int>(grid), wpb, st.stream)));
+            rc.wide ? sgk::launch_wide_align(p, static_cast<int>(grid), st.stream)
+                    : sgk::launch_window_align(rc.L, p, static_cast<int>(grid), wpb, st.stream)));
         ++launches;
     }
     SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
@@ -908,9 +926,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             mark("start");
             // streamed: the first round of lanes takes pairs from the front of memory
             const bool streamed = !getenv("SG_NO_STREAM");
-            const int64_t split = streamed ? k1_grid(st, rcfg, s.hi - s.lo) *
-                                                 sgk::k1_warps_per_block(rcfg.L) * 32
-                                           : 0;
+            const int64_t split = streamed ? pairs_in_flight(st, rcfg, s.hi - s.lo) : 0;
             prep_shard(s, prep[d], mixed, split);
             mark("prep");
             o.h2d_bytes = upload_shard(st, s, prep[d], streamed);
@@ -1252,7 +1268,7 @@ int sg_session_fetch(sg_session* s, sg_results* out) {
 int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* limbs) {
     if (lanes) *lanes = s->st.lanes;
     if (sms) *sms = s->st.sms;
-    if (limbs) *limbs = s->rc.L;
+    if (limbs) *limbs = s->rc.wide ? (s->rc.wcap + 31) / 32 : s->rc.L;
     return SG_OK;
 }
 

@@ -1,0 +1,474 @@
+// K6 wide_align: GenASM-DC + GenASM-TB + window loop for windows wider than
+// 128 bits: W in (128, 1024] and single windows of up to 1024 characters
+// (BitVector::kMaxBits, proj/include/scrooge/bitvec.hpp:29). Hand-written for
+// sm_100a. Design: DESIGN.md §3.6.
+//
+//  * One warp aligns one pair; lane l holds limb l of every bit vector
+//    (32 lanes x 32 bits = 1024). Logical position q = j + 32L - m_w
+//    (right-aligned, L = ceil(m_w / 32)) lives in lane q / 32, machine bit
+//    31 - q % 32, so the end-of-pattern boundary bit (dp.hpp:145-154) enters
+//    at the LSB of lane L-1, and a DP shift is one shuffle (the carry from
+//    lane l+1) plus one funnel shift.
+//  * DC runs in chunks of 4 rows as a skewed wavefront (row r one column
+//    behind row r-1), like K1: the 4 cells of a step are independent. Each
+//    row's shifted value serves twice: as its own match term in the next
+//    column and as the insertion term of the row below (dp.cpp:187-211 with
+//    S(i,d) = I(i+1,d)), so a cell costs one shuffle. The last row of a chunk
+//    is parked per column in L2-resident scratch for the next chunk.
+//  * Traceback events are the same as K1's, kept in full
+//    width for every column the traceback can reach (all columns of a final
+//    window, W - O otherwise): X |= R & ~shl1(R[i+1][d]), Y |= R & ~R[i+1][d].
+//  * The traceback runs on all lanes in lock step (uniform loads); lane 0
+//    writes the run bytes. Outputs are K1's (distance, windows, status, run
+//    bytes, counters), so K2/K3 and the host path are shared.
+#include "window_align.cuh"
+
+#include <cuda_runtime.h>
+
+namespace sgk {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarps = 4;            // warps per block (independent)
+constexpr int kR = 4;                // rows per chunk
+constexpr int kTxtWords = 1024 / 4 + 8;  // text codes of a window, 1 byte per column
+constexpr int kWarpSmem = 5 * 32 + kTxtWords;  // pattern masks [5][32] + text codes
+
+// R[n][d] of the init column (dp.cpp:146,179): ones(m).shl(min(d, m)), i.e.
+// the last d logical positions cleared (positions left of the pattern are
+// don't-care). d < 0: all ones.
+__device__ __forceinline__ uint32_t init_word(int d, int L, int lane) {
+    if (d < 0) return ~0u;
+    const int cut = 32 * (L - lane) - d;  // positions p < cut of this limb stay set
+    return cut >= 32 ? ~0u : cut <= 0 ? 0u : ~0u << (32 - cut);
+}
+
+// shl1 with boundary bit b entering at the end of the pattern (lane L-1).
+__device__ __forceinline__ uint32_t shl1(uint32_t x, bool last, bool b) {
+    const uint32_t nb = __shfl_down_sync(kFull, x, 1);
+    return __funnelshift_l(last ? (b ? 0x80000000u : 0u) : nb, x, 1);
+}
+
+// 16 bases (2-bit codes) from base a on, base a in bits 1:0.
+__device__ __forceinline__ uint32_t bases16(const uint32_t* seq, int64_t a) {
+    const int64_t w = a >> 4;
+    return __funnelshift_r(__ldcg(seq + w), __ldcg(seq + w + 1), 2 * static_cast<int>(a & 15));
+}
+
+// 32 bits of a 1-bit-per-base mask from base a on.
+__device__ __forceinline__ uint32_t bits32(const uint32_t* m, int64_t a) {
+    const int64_t w = a >> 5;
+    return __funnelshift_r(__ldcg(m + w), __ldcg(m + w + 1), static_cast<int>(a & 31));
+}
+
+// Even bits of x packed into the low 16 bits.
+__device__ __forceinline__ uint32_t even_bits(uint32_t x) {
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    return (x | (x >> 8)) & 0x0000FFFFu;
+}
+
+// 4 two-bit fields (bits 0..7) -> 4 bytes; 4 bits -> 4 bytes of 0/1.
+__device__ __forceinline__ uint32_t spread4(uint32_t a) {
+    a &= 0xFFu;
+    return (a | (a << 6) | (a << 12) | (a << 18)) & 0x03030303u;
+}
+__device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
+    return (b & 1u) | ((b & 2u) << 7) | ((b & 4u) << 14) | ((b & 8u) << 21);
+}
+
+// Chunk state. Index 0 is row d0-1 (the parked row of the previous chunk, or
+// all ones for d0 = 0); index k = r + 1 is row d0 + r. v: the row's value at
+// its current column; vp: at the column before (to its right); sh: shl1(v)
+// with the boundary bit of the next column; insp: the insertion term the row
+// used at its previous column (its substitution term now); pm: the pattern
+// mask of the row's column (handed down the rows with the wavefront).
+struct Chunk {
+    uint32_t v[kR + 1], vp[kR + 1], sh[kR + 1], insp[kR + 1], pm[kR + 1];
+    uint32_t ax[4], ay[4], ox[4], oy[4];  // events of the 4 columns in flight (by entry step)
+    uint32_t nbr[4];                      // parked row, prefetched 4 columns ahead
+    uint32_t pmn;                         // pattern mask of row 0's next column
+};
+
+struct ChunkGeo {
+    int S0, d0, cap, off;
+    bool last, ors;  // lane L-1; OR the events into the earlier chunks'
+};
+
+// Step s of a chunk (U = s mod 4, static): rows R-1..0 in descending order
+// (each reads its upper neighbour's state from the previous step), the parked
+// row advancing just before row 0.
+template <int U>
+__device__ __forceinline__ void chunk_step(Chunk& S, const ChunkGeo& G, int s,
+                                           const uint32_t* pmv, const uint8_t* txt,
+                                           uint32_t* park, uint32_t* evx, uint32_t* evy, int& fr) {
+#pragma unroll
+    for (int r = kR - 1; r >= 0; --r) {
+        const int i = G.S0 - s + r;
+        if (r == 0 && s <= G.S0) {  // the parked row (d0 - 1) moves to column i
+            S.vp[0] = S.v[0];
+            if (G.d0 > 0) {
+                S.v[0] = S.nbr[U];
+                if (i >= 4) S.nbr[U] = park[(i - 4) * 32];
+            }
+            S.sh[0] = G.d0 > 0 ? shl1(S.v[0], G.last, s + 1 > G.d0 - 1) : ~0u;
+        }
+        if (r > s || i < 0) continue;  // not yet entered / past column 0 (uniform)
+        const int k = r + 1;
+        const int d = G.d0 + r;
+        const int slot = (U - r) & 3;
+        if (r > 0) {
+            S.pm[k] = S.pm[k - 1];
+        } else {
+            S.pm[1] = S.pmn;
+            S.pmn = i >= 1 ? pmv[txt[i - 1] * 32] : ~0u;
+        }
+        const uint32_t ins = S.sh[k - 1], diag = S.vp[k - 1], sub = S.insp[k];
+        const uint32_t se = S.sh[k], east = S.v[k];
+        const uint32_t rn = ins & diag & sub & (se | S.pm[k]);  // dp.cpp:187-211
+        if (i < G.cap) {
+            const uint32_t x = rn & ~se, y = rn & ~east;
+            if (r == 0) {
+                S.ax[slot] = x;
+                S.ay[slot] = y;
+                if (G.ors) {  // earlier chunks' events, consumed when row R-1 leaves
+                    S.ox[slot] = evx[i * 32];
+                    S.oy[slot] = evy[i * 32];
+                } else {
+                    S.ox[slot] = S.oy[slot] = 0u;
+                }
+            } else {
+                S.ax[slot] |= x;
+                S.ay[slot] |= y;
+            }
+        }
+        S.insp[k] = ins;
+        S.vp[k] = east;
+        S.v[k] = rn;
+        S.sh[k] = shl1(rn, G.last, s - r + 1 > d);  // [n - i > d]
+        if (r == kR - 1) {
+            park[i * 32] = rn;
+            if (i < G.cap) {
+                evx[i * 32] = S.ax[slot] | S.ox[slot];
+                evy[i * 32] = S.ay[slot] | S.oy[slot];
+            }
+        }
+        if (i == 0 && fr < 0) {  // bit j = 0 of R[0][d] (dp.cpp:222)
+            const uint32_t w0 = __shfl_sync(kFull, rn, 0);
+            if (!((w0 >> (31 - G.off)) & 1u)) fr = r;
+        }
+    }
+}
+
+// One chunk: rows d0..d0+3 over columns n_w-1..0. Returns the first row r of
+// the chunk with bit j = 0 of R[0][d0+r] clear, or -1.
+__device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0, int cap,
+                                     const uint32_t* pmv, const uint8_t* txt, uint32_t* park,
+                                     uint32_t* evx, uint32_t* evy, int lane) {
+    Chunk S;
+    ChunkGeo G{n_w - 1, d0, cap, off, last, d0 > 0};
+#pragma unroll
+    for (int k = 0; k <= kR; ++k) {  // every row starts at the init column n
+        const int d = d0 + k - 1;
+        S.v[k] = init_word(d, L, lane);
+        S.vp[k] = S.v[k];
+        S.sh[k] = shl1(S.v[k], last, 0 > d);
+        S.pm[k] = ~0u;
+    }
+#pragma unroll
+    for (int k = 1; k <= kR; ++k) S.insp[k] = S.sh[k - 1];
+    S.insp[0] = ~0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        S.ax[u] = S.ay[u] = S.ox[u] = S.oy[u] = 0u;
+        S.nbr[u] = d0 > 0 && n_w - 1 - u >= 0 ? park[(n_w - 1 - u) * 32] : ~0u;
+    }
+    S.pmn = pmv[txt[n_w - 1] * 32];
+    int fr = -1;
+    const int nsteps = n_w + kR - 1;
+    for (int s = 0; s < nsteps; s += 4) {
+        chunk_step<0>(S, G, s, pmv, txt, park, evx, evy, fr);
+        chunk_step<1>(S, G, s + 1, pmv, txt, park, evx, evy, fr);
+        chunk_step<2>(S, G, s + 2, pmv, txt, park, evx, evy, fr);
+        chunk_step<3>(S, G, s + 3, pmv, txt, park, evx, evy, fr);
+    }
+    return fr;
+}
+
+__global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint32_t* const pmv = smem + wib * kWarpSmem;                      // [5][32]
+    uint8_t* const txt = reinterpret_cast<uint8_t*>(pmv + 5 * 32);     // [4 kTxtWords]
+    uint32_t* const txt32 = pmv + 5 * 32;
+    const long long gwarp = static_cast<long long>(blockIdx.x) * kWarps + wib;
+    const int wcap = P.wcap;
+    uint32_t* const park = P.bnd + gwarp * static_cast<long long>(wide_warp_words(wcap));
+    uint32_t* const evx = park + static_cast<long long>(wcap + 8) * 32;
+    uint32_t* const evy = evx + static_cast<long long>(wcap) * 32;
+    pmv[4 * 32 + lane] = ~0u;  // non-ACGT text matches nothing
+
+    const int W = P.W;
+    const int step_limit = W - P.O;
+    const int K = P.single ? P.k_single : W;  // edit budget: rows 0..K
+
+    for (;;) {
+        unsigned q = 0;
+        if (lane == 0) q = atomicAdd(P.next_pair, 1u);
+        q = __shfl_sync(kFull, q, 0);
+        if (q >= static_cast<unsigned>(P.n_pairs)) break;
+        const int pair = P.order ? P.order[q] : static_cast<int>(q);
+        const int n_tot = P.text_len[pair], m_tot = P.pat_len[pair];
+        const int64_t tbase = P.text_off[pair], pbase = P.pat_off[pair];
+        {   // streamed upload: wait until the pair's sequence words have arrived
+            const int64_t lw = (max(tbase + n_tot, pbase + m_tot) + 15) >> 4;
+            const int64_t cw = lw / P.chunk_words;
+            const int c = cw < P.n_chunks - 1 ? static_cast<int>(cw) : P.n_chunks - 1;
+            while (*reinterpret_cast<const volatile unsigned*>(P.ready + c) == 0u) __nanosleep(1000);
+        }
+        const bool hasn = P.has_n ? P.has_n[pair] != 0 : false;
+        int toff = 0, poff = 0, dist = 0, nwin = 0, status = 0;
+        const int window_cap = 4 * ((n_tot + m_tot) / step_limit + 2);  // aligner.cpp:40
+        uint32_t* outw = P.scratch + (P.bound_off[pair] >> 2);
+        int out_bytes = 0, cur_op = -1, cur_len = 0, acc_n = 0;
+        uint32_t acc = 0;
+        unsigned long long c_stored = 0, c_writes = 0, c_reads = 0, c_rows = 0, c_cells = 0,
+                           c_bequiv = 0;
+        // CIGAR run bytes (op << 6) | (len - 1), as in K1 (cigar.cpp:9-16);
+        // every lane keeps the same state, lane 0 stores
+        auto put_byte = [&](uint32_t b) {
+            acc |= b << (8 * acc_n);
+            ++out_bytes;
+            if (++acc_n == 4) {
+                if (lane == 0) *outw = acc;
+                ++outw;
+                acc = 0;
+                acc_n = 0;
+            }
+        };
+        auto emit = [&](int op, int len) {  // len >= 1
+            if (op == cur_op && cur_len + len <= 64) {
+                cur_len += len;
+                return;
+            }
+            if (op == cur_op) {
+                len -= 64 - cur_len;
+                cur_len = 64;
+            }
+            if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
+            while (len > 64) {
+                put_byte((static_cast<uint32_t>(op) << 6) | 63u);
+                len -= 64;
+            }
+            cur_op = op;
+            cur_len = len;
+        };
+
+        while (status == 0) {
+            // ---- next logical window (aligner.cpp:44-64; single: aligner.cpp:87-112)
+            const int n_rem = n_tot - toff, m_rem = m_tot - poff;
+            if (n_rem == 0 || m_rem == 0) {
+                if (n_rem + m_rem > 0) {  // aligner.cpp:48-57
+                    emit(n_rem == 0 ? 2 : 3, n_rem + m_rem);
+                    dist += n_rem + m_rem;
+                }
+                break;
+            }
+            const bool fin = P.single || (n_rem <= W && m_rem <= W);
+            const int n_w = P.single ? n_rem : min(W, n_rem);
+            const int m_w = P.single ? m_rem : min(W, m_rem);
+            const int limit = fin ? -1 : step_limit;
+            const int L = (m_w + 31) >> 5;
+            const int off = 32 * L - m_w;
+            const bool last = lane == L - 1;
+            const int cap = limit < 0 ? n_w : min(n_w, limit);
+
+            // ---- pattern masks (dp.cpp:8-21): bit = 0 iff pattern base == code
+            {
+                const int js = lane == 0 ? 0 : 32 * lane - off;  // first base of this limb
+                const int sh = lane == 0 ? off : 0;               // lane 0: j = 0 sits at p = off
+                uint32_t lo = 0u, hi = 0u, nn = ~0u;              // lanes >= L: all ones
+                if (lane < L) {
+                    const int64_t a = pbase + poff + js;
+                    const uint32_t w0 = bases16(P.seq, a), w1 = bases16(P.seq, a + 16);
+                    lo = __brev(even_bits(w0) | (even_bits(w1) << 16)) >> sh;
+                    hi = __brev(even_bits(w0 >> 1) | (even_bits(w1 >> 1) << 16)) >> sh;
+                    nn = hasn ? __brev(bits32(P.nmask, a)) >> sh : 0u;
+                    if (sh) nn |= ~(~0u >> sh);  // positions left of the pattern: don't care
+                }
+                pmv[0 * 32 + lane] = lo | hi | nn;
+                pmv[1 * 32 + lane] = ~lo | hi | nn;
+                pmv[2 * 32 + lane] = lo | ~hi | nn;
+                pmv[3 * 32 + lane] = ~lo | ~hi | nn;
+            }
+            // ---- text codes, 1 byte per column (non-ACGT -> 4)
+            for (int i0 = 16 * lane; i0 < n_w; i0 += 512) {
+                const int64_t a = tbase + toff + i0;
+                const uint32_t w = bases16(P.seq, a);
+                const uint32_t nb = hasn ? bits32(P.nmask, a) : 0u;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    uint32_t c = spread4(w >> (8 * g));
+                    const uint32_t nm = spread4bits(nb >> (4 * g)) * 0xFFu;
+                    c = (c & ~nm) | (0x04040404u & nm);
+                    txt32[(i0 >> 2) + g] = c;
+                }
+            }
+            __syncwarp();
+
+            // ---- GenASM-DC (dp.cpp:104-231), chunks of 4 rows until d_opt (ET) or row K
+            int found_d = -1;
+            for (int d0 = 0;; d0 += kR) {
+                const int fr = dc_chunk(n_w, L, off, last, d0, cap, pmv + lane, txt, park + lane,
+                                        evx + lane, evy + lane, lane);
+                if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
+                if ((P.et && found_d >= 0) || d0 + kR > K) break;
+            }
+            __syncwarp();  // the events are read across lanes below
+
+            // single window with D(0, 0) > k: not found (batch.cpp:57-62)
+            const bool not_found = P.single && found_d < 0;
+            if (found_d < 0 && !not_found) status = kStInternal | kDetNoStep;  // aligner.cpp:69-70
+            {   // reference counters for this window (dp.cpp:23-37,58-75,225-228)
+                const int rows_ref = P.et && found_d >= 0 ? found_d + 1 : K + 1;
+                int pol = P.policy;
+                if (limit < 0 && pol == 2) pol = 1;  // final window: DENT -> SENE
+                int keep_cols = n_w + 1, keep_bits = m_w;
+                if (pol == 2) {
+                    keep_cols = min(n_w, step_limit) + 1;
+                    keep_bits = min(m_w, step_limit + 1);
+                }
+                const unsigned long long slots = pol == 0 ? 3ull : 1ull;
+                c_stored += static_cast<unsigned long long>(rows_ref) * keep_cols * keep_bits * slots;
+                c_writes += static_cast<unsigned long long>(rows_ref) * keep_cols * slots;
+                c_rows += rows_ref;
+                c_cells += static_cast<unsigned long long>(rows_ref) * n_w;
+                c_bequiv += 3ull * (n_w + 1) * static_cast<unsigned long long>(K + 1) * m_w;
+            }
+            if (not_found) {
+                dist = -1;
+                ++nwin;
+                break;
+            }
+            if (status) break;
+
+            // ---- GenASM-TB (traceback.cpp:56-113) over the events: runs of
+            // matches at once (Match <=> t_i == p_j, both ACGT), at a mismatch
+            // Sub > Del > Ins from the events
+            int i = 0, j = 0, d = found_d, steps = 0;
+            const int lim = limit >= 0 ? limit : 0x3FFFFFFF;
+            unsigned reads = 0;
+            for (;;) {
+                int rem = lim - steps;
+                if (rem == 0 || i == n_w || j == m_w) break;
+                const int64_t at = tbase + toff + i, ap = pbase + poff + j;
+                uint32_t x = bases16(P.seq, at) ^ bases16(P.seq, ap);
+                x = (x | (x >> 1)) & 0x55555555u;  // bit 2k: base k differs
+                if (hasn) {
+                    uint32_t s = (bits32(P.nmask, at) | bits32(P.nmask, ap)) & 0xFFFFu;
+                    s = (s | (s << 8)) & 0x00FF00FFu;
+                    s = (s | (s << 4)) & 0x0F0F0F0Fu;
+                    s = (s | (s << 2)) & 0x33333333u;
+                    s = (s | (s << 1)) & 0x55555555u;
+                    x |= s;  // non-ACGT bases never match
+                }
+                const int run = __clz(__brev(x)) >> 1;  // 16 when all 16 bases match
+                const int k = min(min(run, rem), min(n_w - i, m_w - j));
+                if (k > 0) {
+                    reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
+                    i += k;
+                    j += k;
+                    steps += k;
+                    rem -= k;
+                    emit(0, k);
+                }
+                if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w) continue;
+                const int qq = j + off;
+                const uint32_t bit = 0x80000000u >> (qq & 31);
+                const uint32_t ex = evx[i * 32 + (qq >> 5)], ey = evy[i * 32 + (qq >> 5)];
+                const int op = ex & bit ? 1 : (ey & bit ? 3 : 2);
+                if (d == 0) {
+                    status = kStInternal | kDetNoStep;  // traceback.cpp:105-106
+                    break;
+                }
+                reads += 3u;
+                i += op != 2;
+                j += op != 3;
+                --d;
+                ++dist;
+                ++steps;
+                emit(op, 1);
+            }
+            {   // one side consumed: a single run of indels (traceback.cpp:76-86)
+                const int rem = lim - steps;
+                if (status == 0 && rem > 0 && !(i == n_w && j == m_w)) {
+                    const int op = i == n_w ? 2 : 3;
+                    const int left = i == n_w ? m_w - j : n_w - i;
+                    if (d != left) status = kStInternal | (i == n_w ? kDetBudgetI : kDetBudgetD);
+                    const int k = min(rem, left);
+                    i += op != 2 ? k : 0;
+                    j += op != 3 ? k : 0;
+                    d -= k;
+                    dist += k;
+                    steps += k;
+                    emit(op, k);
+                }
+            }
+            if (!P.single) c_reads += reads;  // single window: counted before TB (aligner.cpp:98-99)
+            if (limit < 0 && d != 0 && status == 0) status = kStInternal | kDetLeftover;
+            toff += i;
+            poff += j;
+            ++nwin;
+            if (nwin > window_cap) status = kStInternal | kDetWatchdog;
+        }
+
+        // ---- finish the pair
+        if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
+        if (lane == 0) {
+            if (acc_n) *outw = acc;
+            P.distance[pair] = dist;
+            P.windows[pair] = nwin;
+            P.status[pair] = status;
+            P.out_bytes[pair] = out_bytes;
+            if (P.counters) {
+                uint64_t* c = P.counters + 7ll * pair;
+                c[0] = c_stored;
+                c[1] = c_writes;
+                c[2] = c_reads;
+                c[3] = c_rows;
+                c[4] = c_cells;
+                c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
+                c[6] = c_bequiv;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+size_t wide_smem_bytes() { return static_cast<size_t>(kWarpSmem) * 4 * kWarps; }
+int wide_warps_per_block() { return kWarps; }
+
+int wide_max_blocks_per_sm() {
+    int blocks = 0;
+    cudaFuncSetAttribute(k6_wide_align, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(wide_smem_bytes()));
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &blocks, k6_wide_align, 32 * kWarps, wide_smem_bytes());
+    return e == cudaSuccess ? blocks : 0;
+}
+
+int launch_wide_align(const AlignParams& p, int grid, void* stream) {
+    const size_t smem = wide_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k6_wide_align, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    k6_wide_align<<<grid, 32 * kWarps, smem, static_cast<cudaStream_t>(stream)>>>(p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace sgk

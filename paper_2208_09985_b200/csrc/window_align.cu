@@ -376,7 +376,6 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
     }
 #define SG_STEP(U)                                                                           \
     if (!DRAIN || (U) + 1 < R) {                                                             \
-        const int col0 = col_top - (U);                                                      \
         uint32_t pm0[L], north0[L];                                                          \
         _Pragma("unroll") for (int l = 0; l < L; ++l) {                                      \
             pm0[l] = F.pmn[l];                                                               \

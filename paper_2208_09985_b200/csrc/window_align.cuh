@@ -72,6 +72,7 @@ struct AlignParams {
     const unsigned int* ready;  // [n_chunks] sequence-word chunk has arrived (streamed upload)
     int64_t chunk_words;
     int32_t n_chunks;
+    int32_t wcap;             // K6: widest window (columns) a warp's scratch holds
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
@@ -85,6 +86,18 @@ size_t bnd_scratch_bytes(int L, long long total_warps);
 int k1_warps_per_block(int L);
 size_t k1_smem_bytes(int L);
 int k1_max_blocks_per_sm(int L);
+
+// K6 (csrc/wide_align.cu): one warp per pair, for windows wider than 128 bits
+// (W <= 1024, single windows <= 1024 characters). Scratch per warp, in words:
+// parked row [wcap + 8][32], traceback events X and Y [wcap][32] each.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline long long wide_warp_words(int wcap) { return (3LL * wcap + 8) * 32; }
+int launch_wide_align(const AlignParams& p, int grid, void* stream);
+int wide_warps_per_block();
+size_t wide_smem_bytes();
+int wide_max_blocks_per_sm();
 
 // K2/K3: exclusive scan of the per-pair run byte counts (dense_off has n+1
 // entries, the total last) and compaction of the bounded run regions into one

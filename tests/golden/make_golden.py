@@ -127,6 +127,53 @@ def main():
                  "--W", "64", "--O", "33", "--sene", str(s), "--dent", "0", "--et", str(e)],
                 f"single_k{k}_s{s}e{e}.tsv")
 
+    wide()
+
+
+def wide():
+    """Windows wider than 128 bits (K6): W up to 1024 (AlignerConfig::validate,
+    proj/src/aligner.cpp:8-18) and single windows of up to 1024 characters."""
+    if not os.path.exists(REF_TOOL):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+    kat_tsv = os.path.join(HERE, "kat_pairs.tsv")
+    for (W, O) in [(129, 64), (200, 199), (256, 100), (512, 200), (1024, 400), (1024, 0)]:
+        ref(["align", "--input", kat_tsv, *cfg_flags(W, O)], f"kat_W{W}_O{O}.tsv")
+    ref(["align", "--input", kat_tsv, *cfg_flags(256, 100, 0, 0, 0)], "kat_W256_O100_s0d0e0.tsv")
+    ref(["synth", "--cfg", "4", "--count", "12", "--hash", *cfg_flags(256, 96)], "cfg4_W256_O96.tsv")
+    for bits in (0, 3, 5, 7):
+        s, d, e = bits & 1, (bits >> 1) & 1, (bits >> 2) & 1
+        ref(["synth", "--cfg", "4", "--first", "1000", "--count", "3", "--hash",
+             *cfg_flags(256, 96, s, d, e)], f"cfg4_W256_O96_s{s}d{d}e{e}.tsv")
+    ref(["synth", "--cfg", "4", "--count", "4", "--hash", *cfg_flags(1024, 400)],
+        "cfg4_W1024_O400.tsv")
+
+    rng = random.Random(8713)
+    single = [("acgt_acga", "ACGT", "ACGA"), ("far", "AAAAAAAA", "CCCCCCCC")]
+    for k in range(24):  # random pairs, lengths up to 1024, some with N
+        single.append((f"r{k}", rand_seq(rng, rng.randint(100, 1024), "ACGTN" if k % 6 == 0 else "ACGT"),
+                       rand_seq(rng, rng.randint(100, 1024))))
+    for k in range(36):  # a read and its mutated copy
+        base = rand_seq(rng, rng.randint(129, 1000))
+        read = list(base)
+        for _ in range(max(1, len(read) // rng.choice((6, 12, 40)))):
+            pos = rng.randrange(len(read))
+            r = rng.random()
+            if r < 0.4:
+                read[pos] = rng.choice("ACGT")
+            elif r < 0.7:
+                read.insert(pos, rng.choice("ACGT"))
+            elif len(read) > 1:
+                del read[pos]
+        single.append((f"m{k}", base, "".join(read)[:1024]))
+    single.append(("max", rand_seq(rng, 1024), rand_seq(rng, 1024)))
+    write_pairs("single_wide_pairs.tsv", single)
+    single_tsv = os.path.join(HERE, "single_wide_pairs.tsv")
+    for k in (16, 300, 1024):
+        for s, e in ((1, 1), (0, 0)):
+            ref(["align", "--input", single_tsv, "--mode", "single", "--k", str(k),
+                 "--W", "64", "--O", "33", "--sene", str(s), "--dent", "0", "--et", str(e)],
+                f"single_wide_k{k}_s{s}e{e}.tsv")
+
 
 if __name__ == "__main__":
-    sys.exit(main())
+    sys.exit(wide() if sys.argv[1:] == ["wide"] else main())

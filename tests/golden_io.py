@@ -72,12 +72,15 @@ def run_count(cigar: str) -> int:
     return len(re.findall(r"\d+[=XID]", cigar))
 
 
-_SINGLE = re.compile(r"single_k(\d+)_s(\d)e(\d)\.tsv$")
+_SINGLE = re.compile(r"single_(wide_)?k(\d+)_s(\d)e(\d)\.tsv$")
 
 
-def single_pairs():
+def single_pairs(name="single_k0_s1e1.tsv"):
+    """Pairs of a single-window result file: single_pairs.tsv (lengths <= 128)
+    or single_wide_pairs.tsv (lengths up to 1024)."""
+    src = "single_wide_pairs.tsv" if name.startswith("single_wide_") else "single_pairs.tsv"
     out = {}
-    with open(os.path.join(HERE, "single_pairs.tsv")) as f:
+    with open(os.path.join(HERE, src)) as f:
         for line in f:
             pid, t, p = line.rstrip("\n").split("\t")
             out[pid] = (t, p)
@@ -87,7 +90,7 @@ def single_pairs():
 def single_files():
     """(file, k_single, sene, et) of every single-window result file (dent off)."""
     out = []
-    for path in sorted(glob.glob(os.path.join(HERE, "single_k*.tsv"))):
+    for path in sorted(glob.glob(os.path.join(HERE, "single_*k*_s*e*.tsv"))):
         m = _SINGLE.search(path)
-        out.append((os.path.basename(path), int(m.group(1)), int(m.group(2)), int(m.group(3))))
+        out.append((os.path.basename(path), int(m.group(2)), int(m.group(3)), int(m.group(4))))
     return out

@@ -40,6 +40,7 @@ def test_library_is_built_for_sm100a(sg):
 
 
 @pytest.mark.parametrize("W,O,ok", [(64, 33, True), (64, 24, True), (1, 0, True), (128, 127, True),
+                                    (129, 64, True), (1024, 1023, True), (1025, 0, False),
                                     (32, 32, False), (0, 0, False), (64, -1, False),
                                     (2000, 5, False)])
 def test_config_validation(sg, W, O, ok):
@@ -132,7 +133,11 @@ def test_single_window_length_limits(sg):
     cfg = sg.AlignerConfig(mode="single", dent=False)
     with pytest.raises(sg.InputError, match="toolong.*at most 1024"):
         sg.run_batch([sg.SeqPairRecord("toolong", "A" * 2000, "A" * 2000)], cfg)
-    # the GPU path's own limit: a config error, not a silent fallback
-    with pytest.raises(sg.ConfigError, match="mid.*at most 128"):
-        sg.run_batch([sg.SeqPairRecord("mid", "A" * 300, "A" * 300)], cfg)
+    # up to 1024 characters is valid (K6 on the GPU); without a device the call
+    # fails as a CUDA error, never as a config error or a CPU fallback
+    try:
+        r = sg.run_batch([sg.SeqPairRecord("mid", "A" * 300, "A" * 299)], cfg)
+        assert r.outcomes[0].found and r.outcomes[0].distance == 1
+    except sg.CudaError:
+        pass
     cfg.validate()  # single-window configs without DENT are valid

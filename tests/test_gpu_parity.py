@@ -89,7 +89,10 @@ def _rand(rng, n, alphabet="ACGT"):
 
 CASES = [(1, 0), (2, 1), (3, 0), (5, 2), (7, 6), (16, 8), (31, 15), (32, 0), (32, 31), (33, 1),
          (40, 20), (63, 62), (64, 0), (64, 24), (64, 33), (64, 63), (65, 33), (96, 40),
-         (100, 50), (127, 1), (128, 48), (128, 127)]
+         (100, 50), (127, 1), (128, 48), (128, 127),
+         # K6 (one warp per pair): windows wider than 128 bits
+         (129, 1), (160, 64), (200, 100), (256, 0), (256, 255), (300, 150), (513, 200),
+         (1000, 999), (1024, 400)]
 
 
 @pytest.mark.parametrize("W,Ov", CASES)
@@ -134,6 +137,32 @@ def test_random_pairs_match_oracle(gpu, W, Ov):
             assert res.cigar_string(k) == a.cigar, (k, s, d, e)
             assert int(res.windows[k]) == a.windows
             assert [int(x) for x in res.counters[k]] == [a.counters[n] for n in O.COUNTER_NAMES]
+
+
+WIDE_CROSS = ["kat_W64_O33.tsv", "kat_W16_O0.tsv", "kat_W1_O0.tsv", "kat_W65_O33.tsv",
+              "kat_W128_O65.tsv", "kat_W64_O33_s0d0e0.tsv"]
+
+
+@pytest.mark.parametrize("name", WIDE_CROSS)
+def test_wide_kernel_on_narrow_windows(gpu, monkeypatch, name):
+    """K6 (csrc/wide_align.cu) forced onto windows K1 normally takes: the same
+    reference fixtures must come out (SG_FORCE_WIDE=1 is read per call)."""
+    sg = gpu
+    W, Ov, s, d, e = next(f[1:] for f in G.kat_files() if f[0] == name)
+    monkeypatch.setenv("SG_FORCE_WIDE", "1")
+    pairs = G.kat_pairs()
+    rows = G.read_golden(name)
+    codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
+                                     [sg.encode_sequence(pairs[r["id"]][1]) for r in rows])
+    res = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
+    for k, row in enumerate(rows):
+        _compare(res, k, row)
+    # and on a BASELINE config (cfg2 head: 3000 Illumina-like pairs)
+    if name == "kat_W64_O33.tsv":
+        rows = G.read_golden("cfg2_head.tsv")
+        res = sg.align_packed(_cfg(sg, 64, 24), sg.synth_packed(2, 0, len(rows)))
+        for k, row in enumerate(rows):
+            _compare(res, k, row)
 
 
 def test_pairs_within_one_window_are_exact(gpu):
@@ -233,7 +262,7 @@ def test_reference_single_window(gpu, name, k, s, e):
     # align_single_window (proj/src/aligner.cpp:87-112), run_batch's found flag
     # (batch.cpp:47-62): exact alignments, "not found" past k, reference counters
     sg = gpu
-    pairs = G.single_pairs()
+    pairs = G.single_pairs(name)
     rows = G.read_golden(name)
     cfg = sg.AlignerConfig(W=64, O=33, sene=bool(s), dent=False, early_termination=bool(e),
                            mode="single", k_single=k)

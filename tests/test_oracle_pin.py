@@ -86,7 +86,7 @@ def test_synth_matches_reference_generator_contract():
 def test_oracle_matches_reference_single_window(name, k, s, e):
     # align_single_window (proj/src/aligner.cpp:87-112): found / not found past k,
     # exact distance and CIGAR, counters taken before the traceback
-    pairs = G.single_pairs()
+    pairs = G.single_pairs(name)
     for row in G.read_golden(name):
         t, p = pairs[row["id"]]
         a = O.align(O.encode(t), O.encode(p), W=64, O=33, sene=s, dent=False, et=e,
