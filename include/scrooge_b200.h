@@ -209,6 +209,55 @@ int sg_read_pairs(const char* input, int format, sg_pair_file* out);
 void sg_pair_file_free(sg_pair_file* f);
 int sg_write_results(const char* path, const sg_pair_file* pairs, const sg_results* res, int json);
 
+/* ---- exact global alignment and the accuracy sweep ------
+ * sg_global_align: the optimal unit-cost global alignment of every pair with
+ * the reference oracle's tie-breaking (oracle::global_align,
+ * proj/src/oracle.cpp:39-89), on `device` (K7). Results as sg_align_packed
+ * (windows = 1, found = 1, counters 0). The reference's guards apply: a
+ * sequence over 10^5 bases, or (n+1)(m+1) > 2^30, is SG_INPUT with its
+ * message (oracle.cpp:43-46). */
+int sg_global_align(const sg_packed_pairs* pairs, int device, sg_results* out);
+
+/* oracle::ScoringParams (proj/include/scrooge/oracle.hpp:14-19) and
+ * oracle::score_cigar (oracle.cpp:91-115) of pair k's CIGAR. */
+typedef struct sg_scoring {
+    int32_t match_bonus, mismatch_penalty, gap_open, gap_extend;
+} sg_scoring;
+void sg_scoring_default(sg_scoring* s); /* 2, 4, 4, 2 */
+int64_t sg_score_cigar(const sg_results* res, int64_t k, const sg_scoring* s);
+/* worst_quantile (proj/src/sweep.cpp:11-19): the ceil(p n)-th lowest score. */
+int sg_worst_quantile(const int64_t* scores, int64_t n, double p, int64_t* out);
+
+/* run_sweep (proj/src/sweep.cpp:40-107) with the GPU for both the aligner
+ * (sg_align_packed per W and combo) and the exact oracle (sg_global_align).
+ * SweepOptions (proj/include/scrooge/sweep.hpp:12-40): */
+typedef struct sg_sweep_options {
+    const int32_t* W_list;
+    int32_t n_W;
+    int32_t o_fixed;        /* OverlapRule: -1 = W/2 + 1 (HalfPlusOne), else this fixed O */
+    const uint8_t* combos;  /* ImprovementCombo per entry: bit 0 sene, bit 1 dent, bit 2 et */
+    int32_t n_combos;
+    sg_scoring scoring;
+    int32_t measure_time;   /* 0: pairs_per_s = 0, for byte-stable reports */
+} sg_sweep_options;
+/* SweepRow (sweep.hpp:42-53). */
+typedef struct sg_sweep_row {
+    int32_t W, O;
+    uint8_t sene, dent, et;
+    int64_t q500, q100, q010, q001;
+    double frac_optimal, mean_rows_frac, stored_bits_ratio, pairs_per_s;
+    int64_t oracle_q500, oracle_q100, oracle_q010, oracle_q001;
+} sg_sweep_row;
+/* rows: n_W * n_combos entries, W-major (the reference's order). Errors as
+ * the reference: SG_INPUT for an empty dataset / W list / combo list or an
+ * oversized pair, SG_CONFIG for an invalid (W, O). */
+int sg_sweep(const sg_sweep_options* opt, const sg_packed_pairs* pairs, const int* devices,
+             int n_devices, sg_sweep_row* rows);
+/* sweep_csv (sweep.cpp:110-127), or with json != 0 the CLI's JSON
+ * (proj/tools/main.cpp:90-111, dump(2)). Returns the length; writes the text
+ * and a NUL into buf when it fits. */
+int64_t sg_sweep_format(const sg_sweep_row* rows, int64_t n_rows, int json, char* buf, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@
 #include <pthread.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -542,4 +543,97 @@ int64_t orc_replay_batch(int64_t n_pairs, const uint8_t* text, const int64_t* te
         bad += jobs[t].bad;
     }
     return bad;
+}
+
+/* ---- exact oracle of the accuracy sweep (proj/src/oracle.cpp, sweep.cpp) ---- */
+
+/* global_align, proj/src/oracle.cpp:39-89 */
+int orc_global_align(const uint8_t* text, int64_t n, const uint8_t* pattern, int64_t m,
+                     orc_result* out, char* err, size_t errlen) {
+    memset(out, 0, sizeof *out);
+    if (n > 100000 || m > 100000)
+        return fail(err, errlen, ORC_INPUT,
+                    "global_align: sequence longer than the 10^5 quadratic-cost guard");
+    if ((n + 1) * (m + 1) > ((int64_t)1 << 30))
+        return fail(err, errlen, ORC_INPUT,
+                    "global_align: pair too large for the exact traceback matrix");
+    uint8_t* move = (uint8_t*)malloc((size_t)((n + 1) * (m + 1)));
+    int* prev = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+    int* cur = (int*)malloc(sizeof(int) * (size_t)(m + 1));
+    if (!move || !prev || !cur) {
+        free(move), free(prev), free(cur);
+        return fail(err, errlen, ORC_INTERNAL, "out of memory");
+    }
+#define AT(i, j) ((size_t)(i) * (size_t)(m + 1) + (size_t)(j))
+    for (int64_t j = 0; j <= m; ++j) {
+        prev[j] = (int)j;
+        move[AT(0, j)] = 3;
+    }
+    for (int64_t i = 1; i <= n; ++i) {
+        cur[0] = (int)i;
+        move[AT(i, 0)] = 2;
+        for (int64_t j = 1; j <= m; ++j) {
+            const int eq = text[i - 1] == pattern[j - 1] && text[i - 1] < 4;
+            int best = prev[j - 1] + (eq ? 0 : 1);
+            uint8_t mv = eq ? 0 : 1;
+            if (prev[j] + 1 < best) best = prev[j] + 1, mv = 2;
+            if (cur[j - 1] + 1 < best) best = cur[j - 1] + 1, mv = 3;
+            cur[j] = best;
+            move[AT(i, j)] = mv;
+        }
+        int* t = prev;
+        prev = cur;
+        cur = t;
+    }
+    out->distance = prev[m];
+    /* backward walk, then the runs re-appended in forward order */
+    cigar_t rev = {0};
+    int64_t i = n, j = m;
+    while (i > 0 || j > 0) {
+        switch (move[AT(i, j)]) {
+            case 0: cigar_append(&rev, '=', 1), --i, --j; break;
+            case 1: cigar_append(&rev, 'X', 1), --i, --j; break;
+            case 2: cigar_append(&rev, 'D', 1), --i; break;
+            default: cigar_append(&rev, 'I', 1), --j; break;
+        }
+    }
+#undef AT
+    free(move), free(prev), free(cur);
+    cigar_t c = {0};
+    for (int64_t k = rev.n - 1; k >= 0; --k) cigar_append(&c, rev.ops[k], rev.lens[k]);
+    free(rev.ops), free(rev.lens);
+    out->found = 1;
+    out->windows = 1;
+    return finish(out, &c, ORC_OK);
+}
+
+/* score_cigar, proj/src/oracle.cpp:91-115 */
+int64_t orc_score_cigar(const orc_result* r, int match_bonus, int mismatch_penalty, int gap_open,
+                        int gap_extend) {
+    int64_t score = 0;
+    char prev_op = 0;
+    for (int64_t k = 0; k < r->n_runs; ++k) {
+        const char op = r->ops[k];
+        const int64_t len = r->lens[k];
+        if (op == '=') score += (int64_t)match_bonus * len;
+        else if (op == 'X') score -= (int64_t)mismatch_penalty * len;
+        else if (op == prev_op) score -= (int64_t)gap_extend * len;
+        else score -= gap_open + (int64_t)gap_extend * len;
+        prev_op = op;
+    }
+    return score;
+}
+
+static int cmp_i64(const void* a, const void* b) {
+    const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+/* worst_quantile, proj/src/sweep.cpp:11-19 */
+int64_t orc_worst_quantile(int64_t* scores, int64_t n, double p) {
+    qsort(scores, (size_t)n, sizeof *scores, cmp_i64);
+    int64_t rank = (int64_t)ceil(p * (double)n);
+    if (rank < 1) rank = 1;
+    if (rank > n) rank = n;
+    return scores[rank - 1];
 }

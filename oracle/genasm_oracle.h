@@ -75,6 +75,18 @@ int64_t orc_replay_batch(int64_t n_pairs, const uint8_t* text, const int64_t* te
 int64_t orc_last_window_count(void);
 void orc_last_window_stats(int32_t* d_opt, int32_t* n_w, int32_t* m_w, int64_t cap);
 
+/* oracle::global_align (proj/src/oracle.cpp:39-89): optimal unit-cost global
+ * alignment, forward DP with the choice order diagonal > delete > insert
+ * (strict improvements only), traceback from (n, m). Fills distance, runs
+ * (windows = 1, found = 1). ORC_INPUT for the reference's size guards. */
+int orc_global_align(const uint8_t* text, int64_t n, const uint8_t* pattern, int64_t m,
+                     orc_result* out, char* err, size_t errlen);
+/* oracle::score_cigar (oracle.cpp:91-115) of a result's runs. */
+int64_t orc_score_cigar(const orc_result* r, int match_bonus, int mismatch_penalty, int gap_open,
+                        int gap_extend);
+/* worst_quantile (proj/src/sweep.cpp:11-19); scores are sorted in place. */
+int64_t orc_worst_quantile(int64_t* scores, int64_t n, double p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,6 +12,10 @@
 //   ref_tool bench  --cfg N --first F --count C --threads T [cfg flags]
 //   ref_tool read --input pairs.tsv | read-fasta --input a.fa,b.fa   parsed pairs
 //   ref_tool cli-tsv --input pairs.tsv [cfg flags]   write_batch_tsv output
+//   ref_tool simulate --count C --length L --rate R --seed S   simulate_pairs TSV
+//   ref_tool global --input pairs.tsv   oracle::global_align + score_cigar per pair
+//   ref_tool sweep --input pairs.tsv --W-list 32,64 --O-rule half+1|fixed:N
+//                  --combos none,sene+dent+et   run_sweep + sweep_csv (no timing)
 // cfg flags: --W w --O o --sene 0|1 --dent 0|1 --et 0|1 --mode windowed|single --k k
 #include <chrono>
 #include <cstdint>
@@ -26,6 +30,10 @@
 #include "scrooge/batch.hpp"
 #include "scrooge/errors.hpp"
 #include "scrooge/io.hpp"
+#include "scrooge/oracle.hpp"
+#include "scrooge/simulate.hpp"
+#include "scrooge/sweep.hpp"
+#include <sstream>
 #include "synth.h"
 
 namespace {
@@ -36,6 +44,10 @@ struct Args {
     long long first = 0, count = -1;
     int threads = 1;
     bool hash = false;
+    int length = 0;
+    double rate = 0;
+    unsigned long long seed = 0;
+    std::string w_list = "32,64", o_rule = "half+1", combos = "none,sene+dent+et";
     scrooge::AlignerConfig config;
 };
 
@@ -61,6 +73,12 @@ Args parse(int argc, char** argv) {
         else if (k == "--count") a.count = std::stoll(val());
         else if (k == "--threads") a.threads = std::stoi(val());
         else if (k == "--hash") a.hash = true;
+        else if (k == "--length") a.length = std::stoi(val());
+        else if (k == "--rate") a.rate = std::stod(val());
+        else if (k == "--seed") a.seed = std::stoull(val());
+        else if (k == "--W-list") a.w_list = val();
+        else if (k == "--O-rule") a.o_rule = val();
+        else if (k == "--combos") a.combos = val();
         else if (k == "--W") a.config.W = std::stoi(val());
         else if (k == "--O") a.config.O = std::stoi(val());
         else if (k == "--sene") a.config.sene = std::stoi(val()) != 0;
@@ -138,6 +156,61 @@ int main(int argc, char** argv) {
             // run_align's TSV output path (main.cpp:152-167): read_pairs, run_batch, write_batch_tsv
             const auto pairs = scrooge::read_pairs(a.input, scrooge::PairFormat::Tsv);
             scrooge::write_batch_tsv(std::cout, pairs, scrooge::run_batch(pairs, a.config, a.threads));
+        } else if (a.cmd == "simulate") {
+            // simulate_pairs (simulate.hpp:24-31) with the default ErrorMix
+            const auto sims = scrooge::simulate_pairs(static_cast<int>(a.count), a.length, a.rate,
+                                                      scrooge::ErrorMix{}, a.seed);
+            std::vector<scrooge::SeqPairRecord> pairs;
+            for (const auto& sp : sims) pairs.push_back(sp.rec);
+            scrooge::write_pairs_tsv(std::cout, pairs);
+        } else if (a.cmd == "global") {
+            const auto pairs = scrooge::read_pairs_tsv(a.input);
+            const scrooge::oracle::ScoringParams sp;
+            for (const auto& p : pairs) {
+                const auto ga = scrooge::oracle::global_align(scrooge::encode_sequence(p.text),
+                                                              scrooge::encode_sequence(p.pattern));
+                const std::string cig = scrooge::cigar_to_string(ga.cigar);
+                std::printf("%s\t%d\t", p.id.c_str(), ga.distance);
+                if (a.hash)
+                    std::printf("%016llx\t%zu", static_cast<unsigned long long>(fnv1a(cig)),
+                                ga.cigar.size());
+                else
+                    std::printf("%s", cig.c_str());
+                std::printf("\t%lld\n", static_cast<long long>(scrooge::oracle::score_cigar(ga.cigar, sp)));
+            }
+        } else if (a.cmd == "sweep") {
+            // the CLI's sweep flow (main.cpp:260-285) with timing off
+            scrooge::SweepOptions options;
+            std::stringstream ws(a.w_list);
+            std::string token;
+            while (std::getline(ws, token, ',')) options.W_list.push_back(std::stoi(token));
+            if (a.o_rule == "half+1") {
+                options.o_rule.kind = scrooge::OverlapRule::Kind::HalfPlusOne;
+            } else {
+                options.o_rule.kind = scrooge::OverlapRule::Kind::Fixed;
+                options.o_rule.fixed = std::stoi(a.o_rule.substr(6));
+            }
+            std::stringstream cs(a.combos);
+            while (std::getline(cs, token, ',')) {
+                if (token == "all") {
+                    for (int bits = 0; bits < 8; ++bits)
+                        options.combos.push_back({(bits & 1) != 0, (bits & 2) != 0, (bits & 4) != 0});
+                    continue;
+                }
+                scrooge::ImprovementCombo combo;
+                std::stringstream parts(token);
+                std::string flag;
+                while (token != "none" && std::getline(parts, flag, '+')) {
+                    if (flag == "sene") combo.sene = true;
+                    else if (flag == "dent") combo.dent = true;
+                    else if (flag == "et") combo.et = true;
+                }
+                options.combos.push_back(combo);
+            }
+            options.threads = a.threads;
+            options.measure_time = false;
+            const auto pairs = scrooge::read_pairs(a.input, scrooge::PairFormat::Tsv);
+            std::cout << scrooge::sweep_csv(scrooge::run_sweep(pairs, options));
         } else if (a.cmd == "synth") {
             const auto pairs = synth_pairs(a);
             print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);

@@ -10,6 +10,7 @@ from .aligner import (  # noqa: F401
     PairOutcome, Results, SeqPairRecord, Session, align, align_codes, align_packed,
     cigar_from_string, cigar_to_string, decode_sequence, encode_sequence, last_transfer_bytes,
     pack, run_batch, synth_codes, synth_packed, write_batch_tsv, PairFile, read_pairs,
-    write_results,
+    write_results, ScoringParams, score_cigar, worst_quantile, global_align,
+    global_align_packed, GlobalAlignment, SweepRow, run_sweep, sweep_csv, sweep_json,
 )
 from .build import LIB as LIBRARY_PATH  # noqa: F401

@@ -24,6 +24,8 @@ EXPORTS = (
     "sg_last_transfer_bytes", "sg_session_create", "sg_session_run", "sg_session_fetch",
     "sg_session_info", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
     "sg_pairs_free", "sg_alu_peak", "sg_read_pairs", "sg_pair_file_free", "sg_write_results",
+    "sg_global_align", "sg_scoring_default", "sg_score_cigar", "sg_worst_quantile", "sg_sweep",
+    "sg_sweep_format",
 )
 
 
@@ -48,6 +50,27 @@ class SgPackedPairs(C.Structure):
 class SgPairFile(C.Structure):
     _fields_ = [("n_pairs", C.c_int64), ("ids", C.POINTER(C.c_char_p)),
                 ("packed", SgPackedPairs), ("_owner", C.c_void_p)]
+
+
+class SgScoring(C.Structure):
+    _fields_ = [("match_bonus", C.c_int32), ("mismatch_penalty", C.c_int32),
+                ("gap_open", C.c_int32), ("gap_extend", C.c_int32)]
+
+
+class SgSweepOptions(C.Structure):
+    _fields_ = [("W_list", C.POINTER(C.c_int32)), ("n_W", C.c_int32), ("o_fixed", C.c_int32),
+                ("combos", C.POINTER(C.c_uint8)), ("n_combos", C.c_int32),
+                ("scoring", SgScoring), ("measure_time", C.c_int32)]
+
+
+class SgSweepRow(C.Structure):
+    _fields_ = [("W", C.c_int32), ("O", C.c_int32), ("sene", C.c_uint8), ("dent", C.c_uint8),
+                ("et", C.c_uint8), ("q500", C.c_int64), ("q100", C.c_int64),
+                ("q010", C.c_int64), ("q001", C.c_int64), ("frac_optimal", C.c_double),
+                ("mean_rows_frac", C.c_double), ("stored_bits_ratio", C.c_double),
+                ("pairs_per_s", C.c_double), ("oracle_q500", C.c_int64),
+                ("oracle_q100", C.c_int64), ("oracle_q010", C.c_int64),
+                ("oracle_q001", C.c_int64)]
 
 
 class SgResults(C.Structure):
@@ -112,6 +135,15 @@ def load(build_if_missing: bool = True):
     L.sg_pair_file_free.argtypes = [P(SgPairFile)]
     L.sg_pair_file_free.restype = None
     L.sg_write_results.argtypes = [C.c_char_p, P(SgPairFile), P(SgResults), C.c_int]
+    L.sg_global_align.argtypes = [P(SgPackedPairs), C.c_int, P(SgResults)]
+    L.sg_scoring_default.argtypes = [P(SgScoring)]
+    L.sg_scoring_default.restype = None
+    L.sg_score_cigar.argtypes = [P(SgResults), C.c_int64, P(SgScoring)]
+    L.sg_score_cigar.restype = C.c_int64
+    L.sg_worst_quantile.argtypes = [P(C.c_int64), C.c_int64, C.c_double, P(C.c_int64)]
+    L.sg_sweep.argtypes = [P(SgSweepOptions), P(SgPackedPairs), P(C.c_int), C.c_int, P(SgSweepRow)]
+    L.sg_sweep_format.argtypes = [P(SgSweepRow), C.c_int64, C.c_int, C.c_char_p, C.c_int64]
+    L.sg_sweep_format.restype = C.c_int64
     _lib = L
     return L
 

@@ -28,7 +28,7 @@ from __future__ import annotations
 import ctypes as C
 import re
 from dataclasses import dataclass, field
-from typing import Iterable, Optional, Sequence
+from typing import Iterable, List, Optional, Sequence
 
 import numpy as np
 
@@ -545,3 +545,183 @@ def write_batch_tsv(f, pairs: Sequence[SeqPairRecord], result: BatchResult) -> N
     """write_batch_tsv (proj/src/batch.cpp:106-113)."""
     for p, o in zip(pairs, result.outcomes):
         f.write(f"{p.id}\t{o.distance}\t{cigar_to_string(o.cigar) if o.found else '*'}\n")
+
+
+# ---------------------------------------------------------------- accuracy sweep
+# SURVEY §8(f4): run_sweep (proj/src/sweep.cpp:40-107) with the GPU exact
+# oracle (K7, sg_global_align) in place of the quadratic CPU global_align.
+
+@dataclass
+class ScoringParams:
+    """oracle::ScoringParams (proj/include/scrooge/oracle.hpp:14-19)."""
+    match_bonus: int = 2
+    mismatch_penalty: int = 4
+    gap_open: int = 4
+    gap_extend: int = 2
+
+    def _c(self) -> _ffi.SgScoring:
+        return _ffi.SgScoring(self.match_bonus, self.mismatch_penalty, self.gap_open,
+                              self.gap_extend)
+
+
+def score_cigar(cigar: Iterable, params: Optional[ScoringParams] = None) -> int:
+    """oracle::score_cigar (proj/src/oracle.cpp:91-115): affine gap score of a CIGAR."""
+    params = params or ScoringParams()
+    score, prev = 0, ""
+    for op, n in cigar:
+        if op not in "=XID":
+            raise InputError(f"score_cigar: unknown op '{op}'")
+        if n <= 0:
+            raise InputError("score_cigar: non-positive run length")
+        if op == "=":
+            score += params.match_bonus * n
+        elif op == "X":
+            score -= params.mismatch_penalty * n
+        elif op == prev:
+            score -= params.gap_extend * n
+        else:
+            score -= params.gap_open + params.gap_extend * n
+        prev = op
+    return score
+
+
+def worst_quantile(scores: Sequence[int], p: float) -> int:
+    """worst_quantile (proj/src/sweep.cpp:11-19), through the library."""
+    arr = (C.c_int64 * len(scores))(*scores)
+    out = C.c_int64()
+    _check(_ffi.load().sg_worst_quantile(arr, len(scores), p, C.byref(out)))
+    return out.value
+
+
+def global_align_packed(batch, device: int = 0) -> Results:
+    """oracle::global_align (proj/src/oracle.cpp:39-89) for every pair, on the GPU (K7)."""
+    res = _ffi.SgResults()
+    _check(_ffi.load().sg_global_align(C.byref(batch.c), device, C.byref(res)))
+    return Results(res)
+
+
+@dataclass
+class GlobalAlignment:
+    distance: int
+    cigar: Cigar
+
+
+def global_align(text, pattern, device: int = 0) -> GlobalAlignment:
+    """oracle::global_align for one pair (codes or strings), on the GPU."""
+    b = pack(CodesBatch.from_lists([encode_sequence(text)], [encode_sequence(pattern)]))
+    r = global_align_packed(b, device)
+    return GlobalAlignment(int(r.distance[0]), r.cigar(0))
+
+
+@dataclass
+class SweepRow:
+    """SweepRow (proj/include/scrooge/sweep.hpp:42-53)."""
+    W: int
+    O: int
+    sene: bool
+    dent: bool
+    et: bool
+    q500: int
+    q100: int
+    q010: int
+    q001: int
+    frac_optimal: float
+    mean_rows_frac: float
+    stored_bits_ratio: float
+    pairs_per_s: float
+    oracle_q500: int
+    oracle_q100: int
+    oracle_q010: int
+    oracle_q001: int
+
+
+_COMBO_FLAGS = {"sene": 1, "dent": 2, "et": 4}
+
+
+def _combo_bits(c) -> int:
+    if isinstance(c, int):
+        return c
+    if isinstance(c, str):
+        bits = 0
+        if c != "none":
+            for f in c.split("+"):
+                if f not in _COMBO_FLAGS:
+                    raise InputError(f"unknown improvement '{f}' (expected sene, dent, et, none or all)")
+                bits |= _COMBO_FLAGS[f]
+        return bits
+    sene, dent, et = c
+    return int(bool(sene)) | (int(bool(dent)) << 1) | (int(bool(et)) << 2)
+
+
+def _rows_c(rows):
+    arr = (_ffi.SgSweepRow * len(rows))()
+    for k, r in enumerate(rows):
+        arr[k] = _ffi.SgSweepRow(r.W, r.O, int(r.sene), int(r.dent), int(r.et), r.q500, r.q100,
+                                 r.q010, r.q001, r.frac_optimal, r.mean_rows_frac,
+                                 r.stored_bits_ratio, r.pairs_per_s, r.oracle_q500,
+                                 r.oracle_q100, r.oracle_q010, r.oracle_q001)
+    return arr
+
+
+def run_sweep(pairs, W_list: Sequence[int] = (32, 64), o_rule="half+1",
+              combos=("none", "sene+dent+et"), scoring: Optional[ScoringParams] = None,
+              devices=None, measure_time: bool = True) -> List[SweepRow]:
+    """run_sweep (proj/src/sweep.cpp:40-107) on the GPU. pairs: SeqPairRecords or a
+    packed batch; o_rule "half+1" or "fixed:<n>" (or an int); combos: "none",
+    "sene+dent+et", ..., "all", or (sene, dent, et) tuples."""
+    if not isinstance(pairs, (PackedBatch, _PackedView)):
+        pairs = list(pairs)
+        n = len(pairs)
+        batch = pack(CodesBatch.from_lists([encode_sequence(p.text) for p in pairs],
+                                           [encode_sequence(p.pattern) for p in pairs])) if n else None
+    else:
+        batch = pairs
+        n = batch.c.n_pairs
+    bits = []
+    for c in combos:
+        if c == "all":
+            bits.extend(range(8))
+        else:
+            bits.append(_combo_bits(c))
+    if isinstance(o_rule, int):
+        o_fixed = o_rule
+    elif o_rule == "half+1":
+        o_fixed = -1
+    elif isinstance(o_rule, str) and o_rule.startswith("fixed:"):
+        o_fixed = int(o_rule[6:])
+    else:
+        raise InputError(f"unknown O rule '{o_rule}'")
+    Ws = (C.c_int32 * len(W_list))(*W_list)
+    cs = (C.c_uint8 * max(len(bits), 1))(*bits)
+    opt = _ffi.SgSweepOptions(Ws, len(W_list), o_fixed, cs, len(bits),
+                              (scoring or ScoringParams())._c(), int(measure_time))
+    rows = (_ffi.SgSweepRow * max(len(W_list) * len(bits), 1))()
+    darr, nd = _devices(devices)
+    _check(_ffi.load().sg_sweep(C.byref(opt), C.byref(batch.c) if n else None, darr, nd, rows))
+    out = []
+    for k in range(len(W_list) * len(bits)):
+        r = rows[k]
+        out.append(SweepRow(r.W, r.O, bool(r.sene), bool(r.dent), bool(r.et), r.q500, r.q100,
+                            r.q010, r.q001, r.frac_optimal, r.mean_rows_frac,
+                            r.stored_bits_ratio, r.pairs_per_s, r.oracle_q500, r.oracle_q100,
+                            r.oracle_q010, r.oracle_q001))
+    return out
+
+
+def _sweep_format(rows: Sequence[SweepRow], json: bool) -> str:
+    arr = _rows_c(rows)
+    L = _ffi.load()
+    n = L.sg_sweep_format(arr, len(rows), int(json), None, 0)
+    buf = C.create_string_buffer(n + 1)
+    L.sg_sweep_format(arr, len(rows), int(json), buf, n + 1)
+    return buf.value.decode()
+
+
+def sweep_csv(rows: Sequence[SweepRow]) -> str:
+    """sweep_csv (proj/src/sweep.cpp:110-127)."""
+    return _sweep_format(rows, False)
+
+
+def sweep_json(rows: Sequence[SweepRow]) -> str:
+    """The CLI's sweep JSON (proj/tools/main.cpp:90-111, dump(2))."""
+    return _sweep_format(rows, True)

@@ -13,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libscrooge_b200.so")
-SOURCES = ["window_align.cu", "wide_align.cu", "host.cu", "peak.cu", "synth.c", "io.cpp"]
+SOURCES = ["window_align.cu", "wide_align.cu", "exact_align.cu", "host.cu", "peak.cu", "synth.c",
+           "io.cpp", "sweep.cpp"]
 CLI = os.path.join(LIB_DIR, "sg_align")  # the align / bench CLI (csrc/sg_align.cpp)
 HEADERS = ["window_align.cuh", "synth.h"]
 NVCC_FLAGS = [

@@ -195,6 +195,7 @@ struct DevState {
     cudaEvent_t copy_go = nullptr;
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
+    DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
     long long grid = 0, lanes = 0;
 
     void init(int dev) {
@@ -212,7 +213,7 @@ struct DevState {
         for (DevBuf* b : {&seq, &nmask, &text_off, &pat_off, &text_len, &pat_len, &has_n, &order,
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
-                          &dense, &scan_tmp})
+                          &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
@@ -1292,6 +1293,158 @@ int sg_debug_phase_cycles(unsigned long long* out8) {
 }
 
 int64_t sg_last_transfer_bytes(int direction) { return direction ? g_last_d2h : g_last_h2d; }
+
+/* oracle::global_align (proj/src/oracle.cpp:39-89) on the GPU: K7, then K2/K3. */
+int sg_global_align(const sg_packed_pairs* pairs, int device, sg_results* out) {
+    std::memset(out, 0, sizeof *out);
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!pairs || pairs->n_pairs < 0 || pairs->n_pairs > INT32_MAX)
+        return set_error(SG_INPUT, "bad pair batch");
+    const int64_t n = pairs->n_pairs;
+    for (int64_t k = 0; k < n; ++k) {  // the reference's guards (oracle.cpp:43-46)
+        const int64_t tl = pairs->text_len[k], pl = pairs->pat_len[k];
+        if (tl > 100000 || pl > 100000)
+            return set_error(SG_INPUT,
+                             "global_align: sequence longer than the 10^5 quadratic-cost guard");
+        if ((tl + 1) * (pl + 1) > (int64_t{1} << 30))
+            return set_error(SG_INPUT, "global_align: pair too large for the exact traceback matrix");
+    }
+    if (device < 0 || sg_device_count() <= device)
+        return set_error(SG_CUDA, "no CUDA device %d (the GPU path has no CPU fallback)", device);
+    try {
+        SG_CUDA_CHECK(cudaSetDevice(device));
+        DevSlot& slot = dev_slot(device, 0);
+        std::lock_guard<std::mutex> lk(slot.mu);
+        if (!slot.st) {
+            slot.st = std::make_unique<DevState>();
+            slot.st->init(device);
+        }
+        DevState& st = *slot.st;
+        const Shard sh{pairs, 0, n};
+        ShardPrep pp;
+        prep_shard(sh, pp, false);
+        upload_shard(st, sh, pp);
+        const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
+        st.distance.ensure(4 * n1);
+        st.out_bytes.ensure(4 * n1);
+        st.scratch.ensure(static_cast<size_t>(std::max<int64_t>(pp.scratch_bytes, 4)));
+        st.dense_off.ensure(8 * (n1 + 1));
+        st.dense.ensure(static_cast<size_t>(std::max<int64_t>(pp.scratch_bytes, 4)));
+        st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
+        // The delta store (16 B per 32 cells) goes in batches of pairs within a
+        // memory budget (SG_EXACT_BUDGET bytes, default 4 GiB; a larger pair runs alone).
+        int64_t budget = int64_t{4} << 30;
+        if (const char* e = getenv("SG_EXACT_BUDGET")) budget = std::max<int64_t>(1, atoll(e));
+        PinBuf soff, hoff;
+        soff.ensure(8 * n1);
+        hoff.ensure(8 * n1);
+        std::vector<int64_t> cut{0};
+        std::vector<int64_t> batch_store, batch_h;
+        {
+            int64_t s_acc = 0, h_acc = 0;
+            for (int64_t k = 0; k < n; ++k) {
+                const int64_t tl = pairs->text_len[k], pl = pairs->pat_len[k];
+                const int64_t sw = ((pl + 31) / 32) * tl;           // uint4 entries
+                const int64_t hw = ((tl + 15) & ~int64_t{15}) + 16;  // bytes
+                if (k > cut.back() && (s_acc + sw) * 16 > budget) {
+                    cut.push_back(k);
+                    batch_store.push_back(s_acc);
+                    batch_h.push_back(h_acc);
+                    s_acc = h_acc = 0;
+                }
+                soff.as<int64_t>()[k] = s_acc;
+                hoff.as<int64_t>()[k] = h_acc;
+                s_acc += sw;
+                h_acc += hw;
+            }
+            cut.push_back(n);
+            batch_store.push_back(s_acc);
+            batch_h.push_back(h_acc);
+        }
+        const int64_t max_store = *std::max_element(batch_store.begin(), batch_store.end());
+        const int64_t max_h = *std::max_element(batch_h.begin(), batch_h.end());
+        st.ex_store.ensure(static_cast<size_t>(std::max<int64_t>(max_store, 1)) * 16);
+        st.ex_hbuf.ensure(static_cast<size_t>(std::max<int64_t>(max_h, 16)));
+        st.ex_store_off.ensure(8 * n1);
+        st.ex_hbuf_off.ensure(8 * n1);
+        if (n) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(st.ex_store_off.p, soff.p, 8 * static_cast<size_t>(n),
+                                          cudaMemcpyHostToDevice, st.stream));
+            SG_CUDA_CHECK(cudaMemcpyAsync(st.ex_hbuf_off.p, hoff.p, 8 * static_cast<size_t>(n),
+                                          cudaMemcpyHostToDevice, st.stream));
+        }
+        int launches = 0;
+        SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
+        for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
+            const int64_t lo = cut[bi], hi = cut[bi + 1];
+            if (hi <= lo) continue;
+            sgk::ExactParams p{};
+            p.seq = st.seq.as<uint32_t>();
+            p.nmask = pp.any_n ? st.nmask.as<uint32_t>() : nullptr;
+            p.text_off = st.text_off.as<int64_t>() + lo;
+            p.pat_off = st.pat_off.as<int64_t>() + lo;
+            p.text_len = st.text_len.as<int32_t>() + lo;
+            p.pat_len = st.pat_len.as<int32_t>() + lo;
+            p.has_n = pp.any_n ? st.has_n.as<uint8_t>() + lo : nullptr;
+            p.n_pairs = static_cast<int32_t>(hi - lo);
+            p.store = static_cast<uint4*>(st.ex_store.p);
+            p.store_off = st.ex_store_off.as<int64_t>() + lo;
+            p.hbuf = static_cast<int8_t*>(st.ex_hbuf.p);
+            p.hbuf_off = st.ex_hbuf_off.as<int64_t>() + lo;
+            p.bound_off = st.bound_off.as<int64_t>() + lo;
+            p.scratch = st.scratch.as<uint8_t>();
+            p.distance = st.distance.as<int32_t>() + lo;
+            p.out_bytes = st.out_bytes.as<int32_t>() + lo;
+            SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_exact_align(p, st.stream)));
+            ++launches;
+        }
+        SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
+        SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_offsets(
+            st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), static_cast<int32_t>(n),
+            st.scan_tmp.p, st.scan_tmp.cap, st.stream)));
+        SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_compact(
+            st.scratch.as<uint32_t>(), st.bound_off.as<int64_t>(), st.dense_off.as<int64_t>(),
+            st.out_bytes.as<int32_t>(), st.dense.as<uint8_t>(), static_cast<int32_t>(n), st.stream)));
+        launches += n > 0 ? 4 : 0;
+        SG_CUDA_CHECK(cudaEventRecord(st.ev[2], st.stream));
+        PinBuf dist, doff;
+        dist.ensure(4 * n1);
+        doff.ensure(8 * (n1 + 1));
+        if (n) {
+            SG_CUDA_CHECK(cudaMemcpyAsync(dist.p, st.distance.p, 4 * static_cast<size_t>(n),
+                                          cudaMemcpyDeviceToHost, st.stream));
+        }
+        SG_CUDA_CHECK(cudaMemcpyAsync(doff.p, st.dense_off.p, 8 * (static_cast<size_t>(n) + 1),
+                                      cudaMemcpyDeviceToHost, st.stream));
+        SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+        const int64_t run_bytes = doff.as<int64_t>()[n];
+        results_alloc(out, n, run_bytes);
+        if (run_bytes)
+            SG_CUDA_CHECK(cudaMemcpy(out->runs, st.dense.p, static_cast<size_t>(run_bytes),
+                                     cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < n; ++k) {
+            out->distance[k] = dist.as<int32_t>()[k];
+            out->windows[k] = 1;
+            out->found[k] = 1;
+            out->cigar_off[k] = doff.as<int64_t>()[k];
+        }
+        out->cigar_off[n] = run_bytes;
+        std::memset(out->counters, 0, 8 * SG_CNT_COUNT * n1);
+        finish_totals(out);
+        float ms = 0, k7 = 0;
+        SG_CUDA_CHECK(cudaEventElapsedTime(&ms, st.ev[0], st.ev[2]));
+        SG_CUDA_CHECK(cudaEventElapsedTime(&k7, st.ev[0], st.ev[1]));
+        out->device_ms = ms;
+        out->kernel_ms = k7;
+        out->gpu_launches = launches;
+        out->align_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return SG_OK;
+    } catch (const Fail& f) {
+        sg_results_free(out);
+        return f.code;
+    }
+}
 
 int sg_synth_packed(int cfg_id, int64_t first, int64_t count, sg_packed_pairs* out) {
     std::memset(out, 0, sizeof *out);

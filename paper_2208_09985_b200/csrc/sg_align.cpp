@@ -7,6 +7,10 @@
 //                  [--threads N] [--output PATH] [--mode windowed|single] [--k K]
 //                  [--json] [--devices 0,1,...]
 //   sg_align bench ...same...   (also prints the throughput report on stderr)
+//   sg_align sweep --input pairs.tsv [--format tsv|fasta-pair] [--W-list 32,64]
+//                  [--O-rule half+1|fixed:N] [--combos none,sene+dent+et|all|...]
+//                  [--threads N] [--report PATH] [--json] [--no-timing] [--devices 0,1,...]
+//                  (the accuracy sweep, main.cpp:218-286, with the GPU exact oracle)
 //
 // Exit codes follow main.cpp:287-299: 1 for input/config errors ("error: ..."),
 // 2 for internal errors ("internal error: ...").
@@ -49,7 +53,7 @@ struct Args {
 Args parse(int argc, char** argv) {
     Args a;
     sg_config_default(&a.cfg);
-    if (argc < 2) fail(SG_INPUT, "usage: sg_align align|bench --input FILE [options]");
+    if (argc < 2) fail(SG_INPUT, "usage: sg_align align|bench|sweep --input FILE [options]");
     a.cmd = argv[1];
     if (a.cmd != "align" && a.cmd != "bench") fail(SG_INPUT, "unknown command '" + a.cmd + "'");
     for (int i = 2; i < argc; ++i) {
@@ -104,7 +108,133 @@ Args parse(int argc, char** argv) {
     return a;
 }
 
+std::vector<int> parse_list(const std::string& flag, const std::string& s) {
+    std::vector<int> out;
+    size_t p = 0;
+    while (p <= s.size()) {
+        const size_t c = s.find(',', p);
+        out.push_back(parse_int(flag, s.substr(p, c == std::string::npos ? c : c - p)));
+        if (c == std::string::npos) break;
+        p = c + 1;
+    }
+    return out;
+}
+
+// Tokens as std::getline(stream, token, delim) yields them: none for an empty
+// string, no trailing empty token after a final delimiter.
+std::vector<std::string> getline_split(const std::string& s, char delim) {
+    std::vector<std::string> out;
+    size_t p = 0;
+    while (p < s.size()) {
+        size_t c = s.find(delim, p);
+        if (c == std::string::npos) c = s.size();
+        out.push_back(s.substr(p, c - p));
+        p = c + 1;
+    }
+    return out;
+}
+
+// parse_combos, main.cpp:48-75
+std::vector<uint8_t> parse_combos(const std::string& s) {
+    std::vector<uint8_t> combos;
+    for (const std::string& token : getline_split(s, ',')) {
+        if (token == "all") {
+            for (int bits = 0; bits < 8; ++bits) combos.push_back(static_cast<uint8_t>(bits));
+            continue;
+        }
+        uint8_t combo = 0;
+        if (token != "none") {
+            for (const std::string& flag : getline_split(token, '+')) {
+                if (flag == "sene") combo |= 1;
+                else if (flag == "dent") combo |= 2;
+                else if (flag == "et") combo |= 4;
+                else
+                    fail(SG_INPUT, "unknown improvement '" + flag +
+                                       "' (expected sene, dent, et, none or all)");
+            }
+        }
+        combos.push_back(combo);
+    }
+    if (combos.empty()) fail(SG_INPUT, "empty improvement combination list");
+    return combos;
+}
+
+int run_sweep(int argc, char** argv) {
+    std::string input, format = "tsv", w_list = "32,64", o_rule = "half+1",
+                combos = "none,sene+dent+et", report;
+    bool json = false, no_timing = false;
+    int threads = 1;
+    std::vector<int> devices;
+    for (int i = 2; i < argc; ++i) {
+        std::string k = argv[i], v;
+        const size_t eq = k.find('=');
+        const bool has_eq = k.rfind("--", 0) == 0 && eq != std::string::npos;
+        if (has_eq) {
+            v = k.substr(eq + 1);
+            k = k.substr(0, eq);
+        }
+        auto val = [&]() -> std::string {
+            if (has_eq) return v;
+            if (i + 1 >= argc) fail(SG_INPUT, k + " requires a value");
+            return argv[++i];
+        };
+        if (k == "--input") input = val();
+        else if (k == "--format") format = val();
+        else if (k == "--W-list") w_list = val();
+        else if (k == "--O-rule") o_rule = val();
+        else if (k == "--combos") combos = val();
+        else if (k == "--threads") threads = parse_int(k, val());
+        else if (k == "--report") report = val();
+        else if (k == "--json") json = true;
+        else if (k == "--no-timing") no_timing = true;
+        else if (k == "--devices") devices = parse_list(k, val());
+        else fail(SG_INPUT, "unknown option '" + k + "'");
+    }
+    if (input.empty()) fail(SG_INPUT, "--input is required");
+    const std::vector<int> Ws = parse_list("--W-list", w_list);
+    int o_fixed = -1;
+    if (o_rule == "half+1") {
+        o_fixed = -1;
+    } else if (o_rule.rfind("fixed:", 0) == 0) {
+        o_fixed = parse_int("--O-rule", o_rule.substr(6));
+    } else {
+        fail(SG_INPUT, "unknown O rule '" + o_rule + "'");
+    }
+    const std::vector<uint8_t> cs = parse_combos(combos);
+    (void)threads;  // the GPU path has no CPU worker pool
+    int fmt;
+    if (format == "tsv") fmt = SG_FORMAT_TSV;
+    else if (format == "fasta-pair") fmt = SG_FORMAT_FASTA_PAIR;
+    else fail(SG_INPUT, "unknown input format '" + format + "' (expected tsv or fasta-pair)");
+    sg_pair_file pf{};
+    check(sg_read_pairs(input.c_str(), fmt, &pf));
+    sg_sweep_options opt{};
+    opt.W_list = Ws.data();
+    opt.n_W = static_cast<int32_t>(Ws.size());
+    opt.o_fixed = o_fixed;
+    opt.combos = cs.data();
+    opt.n_combos = static_cast<int32_t>(cs.size());
+    sg_scoring_default(&opt.scoring);
+    opt.measure_time = !no_timing;
+    std::vector<sg_sweep_row> rows(Ws.size() * cs.size());
+    const int rc = sg_sweep(&opt, &pf.packed, devices.empty() ? nullptr : devices.data(),
+                            static_cast<int>(devices.size()), rows.data());
+    sg_pair_file_free(&pf);
+    check(rc);
+    const int64_t len = sg_sweep_format(rows.data(), static_cast<int64_t>(rows.size()), json, nullptr, 0);
+    std::string text(static_cast<size_t>(len) + 1, '\0');
+    sg_sweep_format(rows.data(), static_cast<int64_t>(rows.size()), json, &text[0], len + 1);
+    text.resize(static_cast<size_t>(len));
+    if (json) text += '\n';
+    FILE* f = report.empty() || report == "-" ? stdout : std::fopen(report.c_str(), "wb");
+    if (!f) fail(SG_INPUT, "cannot write '" + report + "'");
+    std::fwrite(text.data(), 1, text.size(), f);
+    if (f != stdout) std::fclose(f);
+    return 0;
+}
+
 int run(int argc, char** argv) {
+    if (argc >= 2 && std::strcmp(argv[1], "sweep") == 0) return run_sweep(argc, argv);
     const Args a = parse(argc, argv);
     int format;
     if (a.format == "tsv") format = SG_FORMAT_TSV;  // parse_format, main.cpp:35-39

@@ -29,6 +29,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 namespace sgk {
 
 // Per-pair status (low 16 bits = kind as the C ABI's SG_* codes, high = detail).
@@ -98,6 +100,28 @@ int launch_wide_align(const AlignParams& p, int grid, void* stream);
 int wide_warps_per_block();
 size_t wide_smem_bytes();
 int wide_max_blocks_per_sm();
+
+// K7 (csrc/exact_align.cu): optimal global alignment with the reference
+// oracle's tie-breaking (proj/src/oracle.cpp:39-89), one warp per pair.
+struct ExactParams {
+    const uint32_t* seq;       // as AlignParams
+    const uint32_t* nmask;
+    const int64_t* text_off;
+    const int64_t* pat_off;
+    const int32_t* text_len;
+    const int32_t* pat_len;
+    const uint8_t* has_n;
+    int32_t n_pairs;
+    uint4* store;              // per pair [ceil(m/32)][n] x (Pv, Mv, Ph, Mh)
+    const int64_t* store_off;  // in uint4 units
+    int8_t* hbuf;              // per pair: bottom carries between 1024-row stripes
+    const int64_t* hbuf_off;   // bytes, 16-aligned, >= roundup16(n) + 16 per pair
+    const int64_t* bound_off;  // run-byte region of each pair (as K1)
+    uint8_t* scratch;
+    int32_t* distance;
+    int32_t* out_bytes;
+};
+int launch_exact_align(const ExactParams& p, void* stream);
 
 // K2/K3: exclusive scan of the per-pair run byte counts (dense_off has n+1
 // entries, the total last) and compaction of the bounded run regions into one

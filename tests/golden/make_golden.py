@@ -174,6 +174,45 @@ def wide():
                  "--W", "64", "--O", "33", "--sene", str(s), "--dent", "0", "--et", str(e)],
                 f"single_wide_k{k}_s{s}e{e}.tsv")
 
+    sweep()
+
+
+def sweep():
+    """The accuracy sweep (run_sweep, proj/src/sweep.cpp:40-107) and its exact
+    oracle (global_align / score_cigar, proj/src/oracle.cpp:39-115)."""
+    if not os.path.exists(REF_TOOL):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+
+    def sim(count, length, rate, seed):
+        res = subprocess.run([REF_TOOL, "simulate", "--count", str(count), "--length", str(length),
+                              "--rate", str(rate), "--seed", str(seed)],
+                             capture_output=True, text=True, check=True)
+        return [tuple(line.split("\t")) for line in res.stdout.splitlines()]
+
+    # proj/tests/test_harness.cpp:224-258's dataset
+    write_pairs("sweep_sim.tsv", sim(8, 400, 0.05, 15))
+    # a harder mix: long reads (multi-stripe patterns), high error, N bases, tiny pairs
+    rng = random.Random(4242)
+    mix = sim(24, 1500, 0.1, 77) + [(f"l{k}", t, p) for k, (_, t, p) in enumerate(sim(4, 3000, 0.15, 78))]
+    for k in range(8):
+        mix.append((f"n{k}", rand_seq(rng, rng.randint(1, 200), "ACGTN"),
+                    rand_seq(rng, rng.randint(1, 200), "ACGTN")))
+    mix += [("tiny", "A", "T"), ("one", "ACGT", "ACGA"), ("unb", rand_seq(rng, 900), rand_seq(rng, 30))]
+    write_pairs("sweep_mix.tsv", mix)
+    for name in ("sweep_sim", "sweep_mix"):
+        tsv = os.path.join(HERE, name + ".tsv")
+        ref(["global", "--input", tsv], f"global_{name}.tsv")
+    sim_tsv, mix_tsv = os.path.join(HERE, "sweep_sim.tsv"), os.path.join(HERE, "sweep_mix.tsv")
+    ref(["sweep", "--input", sim_tsv], "sweep_sim_default.csv")
+    ref(["sweep", "--input", mix_tsv, "--W-list", "32,64,128,200", "--combos", "all"],
+        "sweep_mix_all.csv")
+    ref(["sweep", "--input", mix_tsv, "--W-list", "48,96", "--O-rule", "fixed:20",
+         "--combos", "sene,dent+et"], "sweep_mix_fixed.csv")
+
 
 if __name__ == "__main__":
-    sys.exit(wide() if sys.argv[1:] == ["wide"] else main())
+    if sys.argv[1:] == ["wide"]:
+        sys.exit(wide())
+    if sys.argv[1:] == ["sweep"]:
+        sys.exit(sweep())
+    sys.exit(main())

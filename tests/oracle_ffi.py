@@ -75,6 +75,12 @@ def lib():
         L.orc_replay_runs.restype = C.c_int64
         L.orc_replay_batch.argtypes = [C.c_int64] + [C.c_void_p] * 9 + [C.c_int]
         L.orc_replay_batch.restype = C.c_int64
+        L.orc_global_align.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64,
+                                       C.POINTER(OrcResult), C.c_char_p, C.c_size_t]
+        L.orc_score_cigar.argtypes = [C.POINTER(OrcResult)] + [C.c_int] * 4
+        L.orc_score_cigar.restype = C.c_int64
+        L.orc_worst_quantile.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_double]
+        L.orc_worst_quantile.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -113,6 +119,28 @@ def align(text: bytes, pattern: bytes, W=64, O=33, sene=True, dent=True, et=True
                     {n: getattr(res.counters, n) for n in COUNTER_NAMES})
     L.orc_result_free(C.byref(res))
     return out
+
+
+def global_align(text: bytes, pattern: bytes, scoring=(2, 4, 4, 2)):
+    """Oracle global_align (proj/src/oracle.cpp:39-89) -> (distance, cigar, score_cigar)."""
+    L = lib()
+    res = OrcResult()
+    err = C.create_string_buffer(512)
+    rc = L.orc_global_align(bytes(text), len(text), bytes(pattern), len(pattern), C.byref(res),
+                            err, len(err))
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    cig = "".join(f"{res.lens[k]}{res.ops[k].decode()}" for k in range(res.n_runs))
+    score = L.orc_score_cigar(C.byref(res), *scoring)
+    out = (res.distance, cig, score)
+    L.orc_result_free(C.byref(res))
+    return out
+
+
+def worst_quantile(scores, p: float) -> int:
+    """worst_quantile (proj/src/sweep.cpp:11-19)."""
+    arr = (C.c_int64 * len(scores))(*scores)
+    return lib().orc_worst_quantile(arr, len(scores), p)
 
 
 def window_stats():
