@@ -297,4 +297,141 @@ inline void write_batch_tsv(std::ostream& os, const std::vector<SeqPairRecord>& 
     }
 }
 
+// ---- exact oracle and accuracy sweep (oracle.hpp, sweep.hpp) on the GPU
+
+namespace oracle {
+
+struct ScoringParams {  // oracle.hpp:14-19
+    int match_bonus = 2;
+    int mismatch_penalty = 4;
+    int gap_open = 4;
+    int gap_extend = 2;
+};
+
+struct GlobalAlignment {  // oracle.hpp:29-32
+    int distance = 0;
+    Cigar cigar;
+};
+
+// global_align (oracle.cpp:39-89): optimal unit-cost alignment, the reference's
+// tie-breaking, computed by K7.
+inline GlobalAlignment global_align(CodeView text, CodeView pattern) {
+    const std::int64_t zero = 0, n = static_cast<std::int64_t>(text.size()),
+                       m = static_cast<std::int64_t>(pattern.size());
+    sg_pairs p{1, text.data(), &zero, &n, pattern.data(), &zero, &m};
+    sg_packed_pairs packed{};
+    check(sg_pack(&p, &packed));
+    detail::Results res;
+    const int rc = sg_global_align(&packed, 0, &res.r);
+    sg_packed_free(&packed);
+    check(rc);
+    GlobalAlignment out;
+    out.distance = static_cast<int>(res.r.distance[0]);
+    out.cigar = detail::cigar_of(res.r, 0);
+    return out;
+}
+
+// score_cigar (oracle.cpp:91-115).
+inline std::int64_t score_cigar(const Cigar& cigar, const ScoringParams& params) {
+    std::int64_t score = 0;
+    char prev_op = '\0';
+    for (const CigarOp& run : cigar) {
+        if (run.op != '=' && run.op != 'X' && run.op != 'I' && run.op != 'D')
+            throw InputError(std::string("score_cigar: unknown op '") + run.op + "'");
+        if (run.len <= 0) throw InputError("score_cigar: non-positive run length");
+        if (run.op == '=') score += std::int64_t{params.match_bonus} * run.len;
+        else if (run.op == 'X') score -= std::int64_t{params.mismatch_penalty} * run.len;
+        else if (run.op == prev_op) score -= std::int64_t{params.gap_extend} * run.len;
+        else score -= params.gap_open + std::int64_t{params.gap_extend} * run.len;
+        prev_op = run.op;
+    }
+    return score;
+}
+
+}  // namespace oracle
+
+struct ImprovementCombo {  // sweep.hpp:12-16
+    bool sene = false;
+    bool dent = false;
+    bool et = false;
+};
+
+struct OverlapRule {  // sweep.hpp:19-24
+    enum class Kind { HalfPlusOne, Fixed } kind = Kind::HalfPlusOne;
+    int fixed = 0;
+    int overlap_for(int W) const { return kind == Kind::HalfPlusOne ? W / 2 + 1 : fixed; }
+};
+
+struct SweepOptions {  // sweep.hpp:26-36
+    std::vector<int> W_list;
+    OverlapRule o_rule;
+    std::vector<ImprovementCombo> combos;
+    oracle::ScoringParams scoring;
+    int threads = 1;
+    bool measure_time = true;
+    std::vector<int> devices;  // GPU devices (empty = device 0); no reference equivalent
+};
+
+using SweepRow = sg_sweep_row;  // sweep.hpp:38-49 (same fields)
+
+struct SweepReport {
+    std::vector<SweepRow> rows;
+};
+
+// worst_quantile (sweep.cpp:11-19).
+inline std::int64_t worst_quantile(std::vector<std::int64_t> scores, double p) {
+    std::int64_t out = 0;
+    check(sg_worst_quantile(scores.data(), static_cast<std::int64_t>(scores.size()), p, &out));
+    return out;
+}
+
+// run_sweep (sweep.cpp:40-107): the GPU aligner and the GPU exact oracle.
+inline SweepReport run_sweep(const std::vector<SeqPairRecord>& pairs, const SweepOptions& options) {
+    const std::size_t n = pairs.size();
+    std::vector<std::int64_t> toff(n), tlen(n), poff(n), plen(n);
+    std::vector<BaseCode> text, pattern;
+    for (std::size_t k = 0; k < n; ++k) {
+        toff[k] = static_cast<std::int64_t>(text.size());
+        tlen[k] = static_cast<std::int64_t>(pairs[k].text.size());
+        poff[k] = static_cast<std::int64_t>(pattern.size());
+        plen[k] = static_cast<std::int64_t>(pairs[k].pattern.size());
+        for (char c : pairs[k].text) text.push_back(encode_base(c));
+        for (char c : pairs[k].pattern) pattern.push_back(encode_base(c));
+    }
+    sg_pairs p{static_cast<std::int64_t>(n), text.data(), toff.data(), tlen.data(),
+               pattern.data(), poff.data(), plen.data()};
+    sg_packed_pairs packed{};
+    if (n) check(sg_pack(&p, &packed));
+    std::vector<std::uint8_t> combos;
+    for (const ImprovementCombo& c : options.combos)
+        combos.push_back(static_cast<std::uint8_t>((c.sene ? 1 : 0) | (c.dent ? 2 : 0) | (c.et ? 4 : 0)));
+    sg_sweep_options o{};
+    o.W_list = options.W_list.data();
+    o.n_W = static_cast<std::int32_t>(options.W_list.size());
+    o.o_fixed = options.o_rule.kind == OverlapRule::Kind::HalfPlusOne ? -1 : options.o_rule.fixed;
+    o.combos = combos.data();
+    o.n_combos = static_cast<std::int32_t>(combos.size());
+    o.scoring = {options.scoring.match_bonus, options.scoring.mismatch_penalty,
+                 options.scoring.gap_open, options.scoring.gap_extend};
+    o.measure_time = options.measure_time ? 1 : 0;
+    SweepReport report;
+    report.rows.resize(options.W_list.size() * combos.size());
+    const int rc = sg_sweep(&o, n ? &packed : nullptr,
+                            options.devices.empty() ? nullptr : options.devices.data(),
+                            static_cast<int>(options.devices.size()), report.rows.data());
+    if (n) sg_packed_free(&packed);
+    check(rc);
+    return report;
+}
+
+// sweep_csv (sweep.cpp:110-127).
+inline std::string sweep_csv(const SweepReport& report) {
+    const std::int64_t nr = static_cast<std::int64_t>(report.rows.size());
+    const std::int64_t len = sg_sweep_format(report.rows.data(), nr, 0, nullptr, 0);
+    std::string s(static_cast<std::size_t>(len) + 1, '\0');
+    sg_sweep_format(report.rows.data(), nr, 0, &s[0], len + 1);
+    s.resize(static_cast<std::size_t>(len));
+    return s;
+}
+
 }  // namespace scrooge_b200
