@@ -25,6 +25,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 namespace sgk {
 namespace {
 
@@ -85,37 +87,84 @@ __device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
 // with the boundary bit of the next column; insp: the insertion term the row
 // used at its previous column (its substitution term now); pm: the pattern
 // mask of the row's column (handed down the rows with the wavefront).
+//
+// Scratch is indexed by the step t = S0 - i at which row 0 enters column i,
+// in groups of 4 steps: word (t / 4) * 128 + lane * 4 + t % 4, so that one
+// lane's 4 columns of a group are one 16-byte load or store.
 struct Chunk {
     uint32_t v[kR + 1], vp[kR + 1], sh[kR + 1], insp[kR + 1], pm[kR + 1];
-    uint32_t ax[4], ay[4], ox[4], oy[4];  // events of the 4 columns in flight (by entry step)
-    uint32_t nbr[4];                      // parked row, prefetched 4 columns ahead
-    uint32_t pmn;                         // pattern mask of row 0's next column
+    uint32_t ax[4], ay[4];  // events of the 4 columns in flight (slot = entry step % 4)
+    uint4 pk0, pk1, pk2;    // parked row: groups g, g+1, g+2 (prefetched two groups ahead)
+    uint4 pst, ex, ey;      // row R-1's values / events of the group being completed
+    uint32_t pmn;           // pattern mask of row 0's next column
 };
+
+template <int C> __device__ __forceinline__ uint32_t& comp(uint4& v) {
+    return C == 0 ? v.x : C == 1 ? v.y : C == 2 ? v.z : v.w;
+}
 
 struct ChunkGeo {
     int S0, d0, cap, off;
     bool last, ors;  // lane L-1; OR the events into the earlier chunks'
 };
 
+#ifdef SG_WIDE_CHECK  // debugging aid: trap on a step outside the warp's scratch
+#define SG_COL(c, lo, hi)                                                                  \
+    do {                                                                                   \
+        if ((c) < (lo) || (c) >= (hi)) {                                                   \
+            printf("K6 index %d outside [%d, %d) at line %d\n", (c), (lo), (hi), __LINE__); \
+            asm volatile("trap;");                                                         \
+        }                                                                                  \
+    } while (0)
+#else
+#define SG_COL(c, lo, hi) do { } while (0)
+#endif
+
+// Step variants. kGeneric: any step (rows outside the window skip, the
+// d_opt test at column 0, per-row capture test). kMainOut / kMainCap: steps
+// with all 4 rows inside the window, none / all of them in the traceback
+// columns (the chunk loop picks them per group of 4 steps).
+enum { kGeneric = 0, kMainOut = 1, kMainCap = 2 };
+
+// Completes the group of steps t = 4g..4g+3 of row R-1: the parked row (and
+// the events: stored in a window's first chunk, OR-ed in later) as one 16-byte
+// access per lane.
+__device__ __forceinline__ void flush_group(const Chunk& S, const ChunkGeo& G, int g, bool ev,
+                                            uint4* park4, uint4* evx4, uint4* evy4) {
+    SG_COL(4 * g, 0, G.S0 + 1);
+    park4[g * 32] = S.pst;
+    if (!ev) return;
+    if (!G.ors) {
+        evx4[g * 32] = S.ex;
+        evy4[g * 32] = S.ey;
+    } else {  // fire-and-forget reductions: no load of the earlier chunks' events
+        unsigned long long* x = reinterpret_cast<unsigned long long*>(evx4 + g * 32);
+        unsigned long long* y = reinterpret_cast<unsigned long long*>(evy4 + g * 32);
+        atomicOr(x, (static_cast<unsigned long long>(S.ex.y) << 32) | S.ex.x);
+        atomicOr(x + 1, (static_cast<unsigned long long>(S.ex.w) << 32) | S.ex.z);
+        atomicOr(y, (static_cast<unsigned long long>(S.ey.y) << 32) | S.ey.x);
+        atomicOr(y + 1, (static_cast<unsigned long long>(S.ey.w) << 32) | S.ey.z);
+    }
+}
+
 // Step s of a chunk (U = s mod 4, static): rows R-1..0 in descending order
 // (each reads its upper neighbour's state from the previous step), the parked
 // row advancing just before row 0.
-template <int U>
+template <int U, int MODE>
 __device__ __forceinline__ void chunk_step(Chunk& S, const ChunkGeo& G, int s,
                                            const uint32_t* pmv, const uint8_t* txt,
-                                           uint32_t* park, uint32_t* evx, uint32_t* evy, int& fr) {
+                                           uint4* park4, uint4* evx4, uint4* evy4, int& fr) {
+    constexpr bool GEN = MODE == kGeneric;
+    constexpr int CS = (U + 1) & 3;  // row R-1 at step s finishes t = s - 3: component CS
 #pragma unroll
     for (int r = kR - 1; r >= 0; --r) {
         const int i = G.S0 - s + r;
-        if (r == 0 && s <= G.S0) {  // the parked row (d0 - 1) moves to column i
+        if (r == 0 && (!GEN || s <= G.S0)) {  // the parked row (d0 - 1) moves to column i
             S.vp[0] = S.v[0];
-            if (G.d0 > 0) {
-                S.v[0] = S.nbr[U];
-                if (i >= 4) S.nbr[U] = park[(i - 4) * 32];
-            }
+            if (G.d0 > 0) S.v[0] = comp<U>(S.pk0);
             S.sh[0] = G.d0 > 0 ? shl1(S.v[0], G.last, s + 1 > G.d0 - 1) : ~0u;
         }
-        if (r > s || i < 0) continue;  // not yet entered / past column 0 (uniform)
+        if (GEN && (r > s || i < 0)) continue;  // not yet entered / past column 0 (uniform)
         const int k = r + 1;
         const int d = G.d0 + r;
         const int slot = (U - r) & 3;
@@ -123,22 +172,17 @@ __device__ __forceinline__ void chunk_step(Chunk& S, const ChunkGeo& G, int s,
             S.pm[k] = S.pm[k - 1];
         } else {
             S.pm[1] = S.pmn;
-            S.pmn = i >= 1 ? pmv[txt[i - 1] * 32] : ~0u;
+            S.pmn = !GEN || i >= 1 ? pmv[txt[i - 1] * 32] : ~0u;
         }
         const uint32_t ins = S.sh[k - 1], diag = S.vp[k - 1], sub = S.insp[k];
         const uint32_t se = S.sh[k], east = S.v[k];
         const uint32_t rn = ins & diag & sub & (se | S.pm[k]);  // dp.cpp:187-211
-        if (i < G.cap) {
+        const bool capt = GEN ? i < G.cap : MODE == kMainCap;
+        if (capt) {
             const uint32_t x = rn & ~se, y = rn & ~east;
             if (r == 0) {
                 S.ax[slot] = x;
                 S.ay[slot] = y;
-                if (G.ors) {  // earlier chunks' events, consumed when row R-1 leaves
-                    S.ox[slot] = evx[i * 32];
-                    S.oy[slot] = evy[i * 32];
-                } else {
-                    S.ox[slot] = S.oy[slot] = 0u;
-                }
             } else {
                 S.ax[slot] |= x;
                 S.ay[slot] |= y;
@@ -149,13 +193,14 @@ __device__ __forceinline__ void chunk_step(Chunk& S, const ChunkGeo& G, int s,
         S.v[k] = rn;
         S.sh[k] = shl1(rn, G.last, s - r + 1 > d);  // [n - i > d]
         if (r == kR - 1) {
-            park[i * 32] = rn;
-            if (i < G.cap) {
-                evx[i * 32] = S.ax[slot] | S.ox[slot];
-                evy[i * 32] = S.ay[slot] | S.oy[slot];
+            comp<CS>(S.pst) = rn;
+            if (MODE != kMainOut) {  // (columns left of the traceback region: never read)
+                comp<CS>(S.ex) = S.ax[slot];
+                comp<CS>(S.ey) = S.ay[slot];
             }
+            if (CS == 3) flush_group(S, G, (s - 3) >> 2, MODE != kMainOut, park4, evx4, evy4);
         }
-        if (i == 0 && fr < 0) {  // bit j = 0 of R[0][d] (dp.cpp:222)
+        if (GEN && i == 0 && fr < 0) {  // bit j = 0 of R[0][d] (dp.cpp:222)
             const uint32_t w0 = __shfl_sync(kFull, rn, 0);
             if (!((w0 >> (31 - G.off)) & 1u)) fr = r;
         }
@@ -165,8 +210,8 @@ __device__ __forceinline__ void chunk_step(Chunk& S, const ChunkGeo& G, int s,
 // One chunk: rows d0..d0+3 over columns n_w-1..0. Returns the first row r of
 // the chunk with bit j = 0 of R[0][d0+r] clear, or -1.
 __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0, int cap,
-                                     const uint32_t* pmv, const uint8_t* txt, uint32_t* park,
-                                     uint32_t* evx, uint32_t* evy, int lane) {
+                                     const uint32_t* pmv, const uint8_t* txt, uint4* park4,
+                                     uint4* evx4, uint4* evy4, int lane) {
     Chunk S;
     ChunkGeo G{n_w - 1, d0, cap, off, last, d0 > 0};
 #pragma unroll
@@ -181,19 +226,39 @@ __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0,
     for (int k = 1; k <= kR; ++k) S.insp[k] = S.sh[k - 1];
     S.insp[0] = ~0u;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        S.ax[u] = S.ay[u] = S.ox[u] = S.oy[u] = 0u;
-        S.nbr[u] = d0 > 0 && n_w - 1 - u >= 0 ? park[(n_w - 1 - u) * 32] : ~0u;
-    }
+    for (int u = 0; u < 4; ++u) S.ax[u] = S.ay[u] = 0u;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    S.pk0 = S.pst = S.ex = S.ey = z;
+    S.pk1 = d0 > 0 ? park4[0] : z;
+    S.pk2 = d0 > 0 ? park4[32] : z;
     S.pmn = pmv[txt[n_w - 1] * 32];
     int fr = -1;
-    const int nsteps = n_w + kR - 1;
+    const int S0 = n_w - 1, nsteps = n_w + kR - 1;
+#define SG_GROUP(MODE)                                                    \
+    chunk_step<0, MODE>(S, G, s, pmv, txt, park4, evx4, evy4, fr);        \
+    chunk_step<1, MODE>(S, G, s + 1, pmv, txt, park4, evx4, evy4, fr);    \
+    chunk_step<2, MODE>(S, G, s + 2, pmv, txt, park4, evx4, evy4, fr);    \
+    chunk_step<3, MODE>(S, G, s + 3, pmv, txt, park4, evx4, evy4, fr);
     for (int s = 0; s < nsteps; s += 4) {
-        chunk_step<0>(S, G, s, pmv, txt, park, evx, evy, fr);
-        chunk_step<1>(S, G, s + 1, pmv, txt, park, evx, evy, fr);
-        chunk_step<2>(S, G, s + 2, pmv, txt, park, evx, evy, fr);
-        chunk_step<3>(S, G, s + 3, pmv, txt, park, evx, evy, fr);
+        if (d0 > 0) {  // parked-row groups g = s/4 (now), g+1, g+2 (prefetch)
+            S.pk0 = S.pk1;
+            S.pk1 = S.pk2;
+            SG_COL(s + 8, 0, S0 + 16);
+            S.pk2 = park4[((s >> 2) + 2) * 32];  // (past the last group: padding)
+        }
+        // all rows inside the window and right of column 0 for the whole group
+        // (column 0 has the d_opt test): steps 3..S0-1
+        const bool full = s >= 3 && s + 3 <= S0 - 1;
+        if (full && S0 - (s + 3) >= cap) {
+            SG_GROUP(kMainOut)
+        } else if (full && S0 - s + 3 < cap) {
+            SG_GROUP(kMainCap)
+        } else {
+            SG_GROUP(kGeneric)
+        }
     }
+#undef SG_GROUP
+    if ((S0 & 3) != 3) flush_group(S, G, S0 >> 2, true, park4, evx4, evy4);  // partial last group
     return fr;
 }
 
@@ -206,9 +271,10 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
     uint32_t* const txt32 = pmv + 5 * 32;
     const long long gwarp = static_cast<long long>(blockIdx.x) * kWarps + wib;
     const int wcap = P.wcap;
-    uint32_t* const park = P.bnd + gwarp * static_cast<long long>(wide_warp_words(wcap));
-    uint32_t* const evx = park + static_cast<long long>(wcap + 8) * 32;
-    uint32_t* const evy = evx + static_cast<long long>(wcap) * 32;
+    uint32_t* const scr = P.bnd + gwarp * static_cast<long long>(wide_warp_words(wcap));
+    uint32_t* const park = scr;                                          // [wcap + 16 steps][32]
+    uint32_t* const evx = scr + static_cast<long long>(wcap + 16) * 32;  // [wcap + 8 steps][32]
+    uint32_t* const evy = evx + static_cast<long long>(wcap + 8) * 32;
     pmv[4 * 32 + lane] = ~0u;  // non-ACGT text matches nothing
 
     const int W = P.W;
@@ -322,8 +388,10 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
             // ---- GenASM-DC (dp.cpp:104-231), chunks of 4 rows until d_opt (ET) or row K
             int found_d = -1;
             for (int d0 = 0;; d0 += kR) {
-                const int fr = dc_chunk(n_w, L, off, last, d0, cap, pmv + lane, txt, park + lane,
-                                        evx + lane, evy + lane, lane);
+                const int fr = dc_chunk(n_w, L, off, last, d0, cap, pmv + lane, txt,
+                                        reinterpret_cast<uint4*>(park) + lane,
+                                        reinterpret_cast<uint4*>(evx) + lane,
+                                        reinterpret_cast<uint4*>(evy) + lane, lane);
                 if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
                 if ((P.et && found_d >= 0) || d0 + kR > K) break;
             }
@@ -388,7 +456,9 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
                 if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w) continue;
                 const int qq = j + off;
                 const uint32_t bit = 0x80000000u >> (qq & 31);
-                const uint32_t ex = evx[i * 32 + (qq >> 5)], ey = evy[i * 32 + (qq >> 5)];
+                const int t = n_w - 1 - i;  // events are stored by entry step
+                const int w = (t >> 2) * 128 + (qq >> 5) * 4 + (t & 3);
+                const uint32_t ex = evx[w], ey = evy[w];
                 const int op = ex & bit ? 1 : (ey & bit ? 3 : 2);
                 if (d == 0) {
                     status = kStInternal | kDetNoStep;  // traceback.cpp:105-106
