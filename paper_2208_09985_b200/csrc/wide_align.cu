@@ -89,8 +89,8 @@ __device__ __forceinline__ uint32_t spread4bits(uint32_t b) {
 // mask of the row's column (handed down the rows with the wavefront).
 //
 // Scratch is indexed by the step t = S0 - i at which row 0 enters column i,
-// in groups of 4 steps: word (t / 4) * 128 + lane * 4 + t % 4, so that one
-// lane's 4 columns of a group are one 16-byte load or store.
+// in groups of 4 steps: word (t / 4) * 4L + lane * 4 + t % 4 (lanes < L only),
+// so that one lane's 4 columns of a group are one 16-byte load or store.
 struct Chunk {
     uint32_t v[kR + 1], vp[kR + 1], sh[kR + 1], insp[kR + 1], pm[kR + 1];
     uint32_t ax[4], ay[4];  // events of the 4 columns in flight (slot = entry step % 4)
@@ -104,8 +104,8 @@ template <int C> __device__ __forceinline__ uint32_t& comp(uint4& v) {
 }
 
 struct ChunkGeo {
-    int S0, d0, cap, off;
-    bool last, ors;  // lane L-1; OR the events into the earlier chunks'
+    int S0, d0, cap, off, L;
+    bool last, ors, act;  // lane L-1; OR the events into the earlier chunks'; lane < L
 };
 
 #ifdef SG_WIDE_CHECK  // debugging aid: trap on a step outside the warp's scratch
@@ -132,14 +132,15 @@ enum { kGeneric = 0, kMainOut = 1, kMainCap = 2 };
 __device__ __forceinline__ void flush_group(const Chunk& S, const ChunkGeo& G, int g, bool ev,
                                             uint4* park4, uint4* evx4, uint4* evy4) {
     SG_COL(4 * g, 0, G.S0 + 1);
-    park4[g * 32] = S.pst;
+    if (!G.act) return;
+    park4[g * G.L] = S.pst;
     if (!ev) return;
     if (!G.ors) {
-        evx4[g * 32] = S.ex;
-        evy4[g * 32] = S.ey;
+        evx4[g * G.L] = S.ex;
+        evy4[g * G.L] = S.ey;
     } else {  // fire-and-forget reductions: no load of the earlier chunks' events
-        unsigned long long* x = reinterpret_cast<unsigned long long*>(evx4 + g * 32);
-        unsigned long long* y = reinterpret_cast<unsigned long long*>(evy4 + g * 32);
+        unsigned long long* x = reinterpret_cast<unsigned long long*>(evx4 + g * G.L);
+        unsigned long long* y = reinterpret_cast<unsigned long long*>(evy4 + g * G.L);
         atomicOr(x, (static_cast<unsigned long long>(S.ex.y) << 32) | S.ex.x);
         atomicOr(x + 1, (static_cast<unsigned long long>(S.ex.w) << 32) | S.ex.z);
         atomicOr(y, (static_cast<unsigned long long>(S.ey.y) << 32) | S.ey.x);
@@ -213,7 +214,7 @@ __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0,
                                      const uint32_t* pmv, const uint8_t* txt, uint4* park4,
                                      uint4* evx4, uint4* evy4, int lane) {
     Chunk S;
-    ChunkGeo G{n_w - 1, d0, cap, off, last, d0 > 0};
+    ChunkGeo G{n_w - 1, d0, cap, off, L, last, d0 > 0, lane < L};
 #pragma unroll
     for (int k = 0; k <= kR; ++k) {  // every row starts at the init column n
         const int d = d0 + k - 1;
@@ -229,8 +230,8 @@ __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0,
     for (int u = 0; u < 4; ++u) S.ax[u] = S.ay[u] = 0u;
     const uint4 z = make_uint4(0u, 0u, 0u, 0u);
     S.pk0 = S.pst = S.ex = S.ey = z;
-    S.pk1 = d0 > 0 ? park4[0] : z;
-    S.pk2 = d0 > 0 ? park4[32] : z;
+    S.pk1 = d0 > 0 && G.act ? park4[0] : z;
+    S.pk2 = d0 > 0 && G.act ? park4[L] : z;
     S.pmn = pmv[txt[n_w - 1] * 32];
     int fr = -1;
     const int S0 = n_w - 1, nsteps = n_w + kR - 1;
@@ -244,7 +245,7 @@ __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0,
             S.pk0 = S.pk1;
             S.pk1 = S.pk2;
             SG_COL(s + 8, 0, S0 + 16);
-            S.pk2 = park4[((s >> 2) + 2) * 32];  // (past the last group: padding)
+            if (G.act) S.pk2 = park4[((s >> 2) + 2) * L];  // (past the last group: padding)
         }
         // all rows inside the window and right of column 0 for the whole group
         // (column 0 has the d_opt test): steps 3..S0-1
@@ -272,9 +273,10 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
     const long long gwarp = static_cast<long long>(blockIdx.x) * kWarps + wib;
     const int wcap = P.wcap;
     uint32_t* const scr = P.bnd + gwarp * static_cast<long long>(wide_warp_words(wcap));
-    uint32_t* const park = scr;                                          // [wcap + 16 steps][32]
-    uint32_t* const evx = scr + static_cast<long long>(wcap + 16) * 32;  // [wcap + 8 steps][32]
-    uint32_t* const evy = evx + static_cast<long long>(wcap + 8) * 32;
+    const int lmax = (wcap + 31) >> 5, wc4 = (wcap + 3) & ~3;  // widest pattern's limbs
+    uint32_t* const park = scr;                                           // [wcap + 16 steps][L]
+    uint32_t* const evx = scr + static_cast<long long>(wc4 + 16) * lmax;  // [wcap + 8 steps][L]
+    uint32_t* const evy = evx + static_cast<long long>(wc4 + 8) * lmax;
     pmv[4 * 32 + lane] = ~0u;  // non-ACGT text matches nothing
 
     const int W = P.W;
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
                 const int qq = j + off;
                 const uint32_t bit = 0x80000000u >> (qq & 31);
                 const int t = n_w - 1 - i;  // events are stored by entry step
-                const int w = (t >> 2) * 128 + (qq >> 5) * 4 + (t & 3);
+                const int w = (t >> 2) * 4 * L + (qq >> 5) * 4 + (t & 3);
                 const uint32_t ex = evx[w], ey = evy[w];
                 const int op = ex & bit ? 1 : (ey & bit ? 3 : 2);
                 if (d == 0) {
