@@ -263,6 +263,166 @@ __device__ __noinline__ int dc_chunk(int n_w, int L, int off, bool last, int d0,
     return fr;
 }
 
+// ---------------------------------------------------------------- rows across lane groups
+//
+// For L <= 8 limbs a single vector leaves lanes idle, so the rows of a chunk
+// are spread over the warp instead: G = 32 / LG groups of LG lanes (G = 4, LG = 8),
+// group g holding row d0 + g (limb l = lane % LG). The groups form a systolic
+// wavefront: at step s group g works on column i = S0 - s + g, receiving the
+// upper row's value, its shifted value and the column's event accumulators
+// from group g-1 by shuffles (4 per step), and shifting its own value within
+// its segment (1 more). Group 0 reads the parked row (value and shifted value)
+// from scratch; group G-1 parks its row and stores the column's events. A step
+// costs every lane one cell instead of four.
+struct GState {
+    uint32_t v, sh, dg, insp, ax, ay, pm, pmn;
+    uint4 pv0, pv1, pv2, ps0, ps1, ps2;  // parked row / its shift: groups g, g+1, g+2 (group 0)
+    uint4 sv, ss, ex, ey;                // group G-1: the t-group being completed
+};
+
+struct GGeo {
+    int S0, d0, cap, off, L, g, l;
+    bool last, act;  // limb L-1; limb < L
+};
+
+template <int LG>
+__device__ __forceinline__ uint32_t shl1g(uint32_t x, bool last, bool b) {
+    const uint32_t nb = __shfl_down_sync(kFull, x, 1, LG);
+    return __funnelshift_l(last ? (b ? 0x80000000u : 0u) : nb, x, 1);
+}
+
+template <int G>
+__device__ __forceinline__ void gflush(const GState& S, const GGeo& Q, int tg, bool ev,
+                                       uint4* pv4, uint4* ps4, uint4* evx4, uint4* evy4) {
+    if (Q.g != G - 1 || !Q.act) return;
+    SG_COL(4 * tg, 0, Q.S0 + 1);
+    pv4[tg * Q.L] = S.sv;
+    ps4[tg * Q.L] = S.ss;
+    if (!ev) return;
+    if (Q.d0 == 0) {
+        evx4[tg * Q.L] = S.ex;
+        evy4[tg * Q.L] = S.ey;
+    } else {
+        unsigned long long* x = reinterpret_cast<unsigned long long*>(evx4 + tg * Q.L);
+        unsigned long long* y = reinterpret_cast<unsigned long long*>(evy4 + tg * Q.L);
+        atomicOr(x, (static_cast<unsigned long long>(S.ex.y) << 32) | S.ex.x);
+        atomicOr(x + 1, (static_cast<unsigned long long>(S.ex.w) << 32) | S.ex.z);
+        atomicOr(y, (static_cast<unsigned long long>(S.ey.y) << 32) | S.ey.x);
+        atomicOr(y + 1, (static_cast<unsigned long long>(S.ey.w) << 32) | S.ey.z);
+    }
+}
+
+template <int G, int U, int MODE>
+__device__ __forceinline__ void gstep(GState& S, const GGeo& Q, int s, const uint32_t* pmv,
+                                      const uint8_t* txt, uint4* pv4, uint4* ps4, uint4* evx4,
+                                      uint4* evy4, int& fr) {
+    constexpr int LG = 32 / G;
+    constexpr bool GEN = MODE == kGeneric;
+    constexpr int CS = (U - (G - 1)) & 3;  // group G-1 finishes t = s - (G-1): component CS
+    const int i = Q.S0 - s + Q.g;
+    uint32_t nv = __shfl_up_sync(kFull, S.v, LG);
+    uint32_t ns = __shfl_up_sync(kFull, S.sh, LG);
+    uint32_t nx = __shfl_up_sync(kFull, S.ax, LG);
+    uint32_t ny = __shfl_up_sync(kFull, S.ay, LG);
+    if (Q.g == 0) {  // row d0 - 1: the parked row (all ones in a window's first chunk)
+        nv = Q.d0 > 0 ? comp<U>(S.pv0) : ~0u;
+        ns = Q.d0 > 0 ? comp<U>(S.ps0) : ~0u;
+        nx = ny = 0u;
+    }
+    S.pm = S.pmn;
+    S.pmn = i >= 1 && i <= Q.S0 + 1 ? pmv[txt[i - 1] * 32] : ~0u;  // next column's mask
+    const bool act = !GEN || (s >= Q.g && i >= 0);
+    const int d = Q.d0 + Q.g;
+    const uint32_t rn = ns & S.dg & S.insp & (S.sh | S.pm);  // dp.cpp:187-211
+    const uint32_t shn = shl1g<LG>(rn, Q.last, s + 1 > Q.d0 + 2 * Q.g);  // [n - i > d]
+    if (act) {
+        const bool capt = GEN ? i < Q.cap : MODE == kMainCap;
+        if (capt) {
+            S.ax = nx | (rn & ~S.sh);
+            S.ay = ny | (rn & ~S.v);
+        }
+        S.v = rn;
+        S.sh = shn;
+        comp<CS>(S.sv) = rn;
+        comp<CS>(S.ss) = shn;
+        if (MODE != kMainOut) {
+            comp<CS>(S.ex) = S.ax;
+            comp<CS>(S.ey) = S.ay;
+        }
+    }
+    S.dg = nv;  // next column: this column's upper row is the diagonal, its shift the substitution
+    S.insp = ns;
+    if (CS == 3 && (!GEN || (s - (G - 1) >= 0 && s - (G - 1) <= Q.S0)))
+        gflush<G>(S, Q, (s - (G - 1)) >> 2, MODE != kMainOut, pv4, ps4, evx4, evy4);
+    (void)d;
+    if (GEN) {  // bit j = 0 of R[0][d] when a row reaches column 0 (dp.cpp:222)
+        const unsigned hit = __ballot_sync(kFull, act && i == 0 && Q.l == 0 &&
+                                                      !((rn >> (31 - Q.off)) & 1u));
+        if (hit && fr < 0) fr = s - Q.S0;
+    }
+}
+
+// One chunk of G rows d0..d0+G-1 (L <= 32 / G). Returns the first row r with
+// bit j = 0 of R[0][d0+r] clear, or -1.
+template <int G>
+__device__ __noinline__ int dc_chunk_g(int n_w, int L, int off, int d0, int cap,
+                                       const uint32_t* pmv, const uint8_t* txt, uint4* pv4,
+                                       uint4* ps4, uint4* evx4, uint4* evy4, int lane) {
+    constexpr int LG = 32 / G;
+    const int g = lane / LG, l = lane % LG;
+    GGeo Q{n_w - 1, d0, cap, off, L, g, l, l == L - 1, l < L};
+    GState S;
+    const int d = d0 + g;
+    S.v = init_word(d, L, l);  // every row starts at the init column n
+    S.sh = shl1g<LG>(S.v, Q.last, 0 > d);
+    {   // row 0's diagonal / substitution terms at its first column: R[n][d0-1]
+        const uint32_t up = init_word(d0 - 1, L, l);
+        const uint32_t ups = shl1g<LG>(up, Q.last, 0 > d0 - 1);
+        S.dg = up;
+        S.insp = ups;
+    }
+    S.ax = S.ay = 0u;
+    S.pm = ~0u;
+    S.pmn = g == 0 ? pmv[txt[n_w - 1] * 32] : ~0u;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    S.pv0 = S.ps0 = S.sv = S.ss = S.ex = S.ey = z;
+    const bool ld = d0 > 0 && g == 0 && Q.act;
+    S.pv1 = ld ? pv4[0] : z;
+    S.ps1 = ld ? ps4[0] : z;
+    S.pv2 = ld ? pv4[L] : z;
+    S.ps2 = ld ? ps4[L] : z;
+    int fr = -1;
+    const int S0 = n_w - 1, nsteps = n_w + G - 1;
+#define SG_GGROUP(MODE)                                                            \
+    gstep<G, 0, MODE>(S, Q, s, pmv, txt, pv4, ps4, evx4, evy4, fr);                \
+    gstep<G, 1, MODE>(S, Q, s + 1, pmv, txt, pv4, ps4, evx4, evy4, fr);            \
+    gstep<G, 2, MODE>(S, Q, s + 2, pmv, txt, pv4, ps4, evx4, evy4, fr);            \
+    gstep<G, 3, MODE>(S, Q, s + 3, pmv, txt, pv4, ps4, evx4, evy4, fr);
+    for (int s = 0; s < nsteps; s += 4) {
+        if (ld) {  // parked-row groups s/4 (now), +1, +2 (prefetch; past the end: padding)
+            S.pv0 = S.pv1;
+            S.pv1 = S.pv2;
+            S.ps0 = S.ps1;
+            S.ps1 = S.ps2;
+            S.pv2 = pv4[((s >> 2) + 2) * L];
+            S.ps2 = ps4[((s >> 2) + 2) * L];
+        }
+        // every group inside the window, none at column 0, for the whole group of steps
+        const bool full = s >= G - 1 && s + 3 <= S0 - 1;
+        if (full && S0 - (s + 3) >= cap) {
+            SG_GGROUP(kMainOut)
+        } else if (full && S0 - s + G - 1 < cap) {
+            SG_GGROUP(kMainCap)
+        } else {
+            SG_GGROUP(kGeneric)
+        }
+    }
+#undef SG_GGROUP
+    // the last t-group, if partial (t = S0 is completed at step S0 + G - 1)
+    if (((S0) & 3) != 3) gflush<G>(S, Q, S0 >> 2, true, pv4, ps4, evx4, evy4);
+    return fr;
+}
+
 __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P) {
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -274,8 +434,9 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
     const int wcap = P.wcap;
     uint32_t* const scr = P.bnd + gwarp * static_cast<long long>(wide_warp_words(wcap));
     const int lmax = (wcap + 31) >> 5, wc4 = (wcap + 3) & ~3;  // widest pattern's limbs
-    uint32_t* const park = scr;                                           // [wcap + 16 steps][L]
-    uint32_t* const evx = scr + static_cast<long long>(wc4 + 16) * lmax;  // [wcap + 8 steps][L]
+    uint32_t* const park = scr;                                             // [wcap + 16 steps][L]
+    uint32_t* const parks = park + static_cast<long long>(wc4 + 16) * lmax;  // its shifts (grouped)
+    uint32_t* const evx = parks + static_cast<long long>(wc4 + 16) * lmax;  // [wcap + 8 steps][L]
     uint32_t* const evy = evx + static_cast<long long>(wc4 + 8) * lmax;
     pmv[4 * 32 + lane] = ~0u;  // non-ACGT text matches nothing
 
@@ -389,13 +550,28 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
 
             // ---- GenASM-DC (dp.cpp:104-231), chunks of 4 rows until d_opt (ET) or row K
             int found_d = -1;
-            for (int d0 = 0;; d0 += kR) {
-                const int fr = dc_chunk(n_w, L, off, last, d0, cap, pmv + lane, txt,
-                                        reinterpret_cast<uint4*>(park) + lane,
-                                        reinterpret_cast<uint4*>(evx) + lane,
-                                        reinterpret_cast<uint4*>(evy) + lane, lane);
+            // L <= 8: the chunk's 4 rows over 4 lane groups of 8; else 4 rows per lane.
+            // (Two groups of 16 for L <= 16 measured 2.5x slower than 4 rows per lane
+            // at W = 512: half the rows per chunk, and one cell per lane per step
+            // leaves the shuffle chain exposed.)
+            const int rows = kR;
+            for (int d0 = 0;; d0 += rows) {
+                int fr;
+                if (L <= 8) {
+                    uint4* const pv4 = reinterpret_cast<uint4*>(park) + lane % 8;
+                    uint4* const ps4 = reinterpret_cast<uint4*>(parks) + lane % 8;
+                    uint4* const ex4 = reinterpret_cast<uint4*>(evx) + lane % 8;
+                    uint4* const ey4 = reinterpret_cast<uint4*>(evy) + lane % 8;
+                    fr = dc_chunk_g<4>(n_w, L, off, d0, cap, pmv + lane % 8, txt, pv4, ps4, ex4,
+                                       ey4, lane);
+                } else {
+                    fr = dc_chunk(n_w, L, off, last, d0, cap, pmv + lane, txt,
+                                  reinterpret_cast<uint4*>(park) + lane,
+                                  reinterpret_cast<uint4*>(evx) + lane,
+                                  reinterpret_cast<uint4*>(evy) + lane, lane);
+                }
                 if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
-                if ((P.et && found_d >= 0) || d0 + kR > K) break;
+                if ((P.et && found_d >= 0) || d0 + rows > K) break;
             }
             __syncwarp();  // the events are read across lanes below
 

@@ -91,13 +91,13 @@ int k1_max_blocks_per_sm(int L);
 
 // K6 (csrc/wide_align.cu): one warp per pair, for windows wider than 128 bits
 // (W <= 1024, single windows <= 1024 characters). Scratch per warp, in words:
-// parked row [wcap + 16][L], traceback events X and Y [wcap + 8][L] each,
-// L = ceil(wcap / 32) limbs.
+// parked row and its shift [wcap + 16][L] each, traceback events X and Y
+// [wcap + 8][L] each, L = ceil(wcap / 32) limbs.
 #ifdef __CUDACC__
 __host__ __device__
 #endif
 inline long long wide_warp_words(int wcap) {  // 128-byte multiple
-    return ((3LL * ((wcap + 3) & ~3) + 32) * ((wcap + 31) / 32) + 31) & ~31LL;
+    return ((4LL * ((wcap + 3) & ~3) + 48) * ((wcap + 31) / 32) + 31) & ~31LL;
 }
 int launch_wide_align(const AlignParams& p, int grid, void* stream);
 int wide_warps_per_block();
