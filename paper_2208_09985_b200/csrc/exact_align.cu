@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(kThreads) k7_exact_align(const ExactParams P) 
         for (int s = 0; s < n + 31; ++s) {
             const int up = __shfl_up_sync(kFull, out, 1);
             const int i = s - lane + 1;  // this lane's column (1-based)
-            if (i < 1 || i > n) continue;
-            int code, hin;
-            if (lane == 0) {
+            const bool valid = i >= 1 && i <= n;
+            int code = up >> 2, hin = (up & 3) - 1;
+            if (lane == 0 && valid) {  // (lane 0 is the only lane whose column is s + 1)
                 const int c = i - 1;
                 if ((c & 15) == 0) {
                     tw_cur = tw_nxt;
@@ -129,24 +129,26 @@ __global__ void __launch_bounds__(kThreads) k7_exact_align(const ExactParams P) 
                                                     : ((c & 15) < 12 ? hc_cur.z : hc_cur.w);
                     hin = static_cast<int>(static_cast<int8_t>((w >> (8 * (c & 3))) & 0xFFu));
                 }
-            } else {
-                code = up >> 2;
-                hin = (up & 3) - 1;
             }
+            // one column of Myers' block step (the lane's math runs every step;
+            // outside its columns the results are dropped)
             uint32_t eq = code == 0 ? e0 : code == 1 ? e1 : code == 2 ? e2 : code == 3 ? e3 : 0u;
             const uint32_t xv = eq | mv;
-            if (hin < 0) eq |= 1u;
+            eq |= hin < 0 ? 1u : 0u;
             const uint32_t xh = (((eq & pv) + pv) ^ pv) | eq;
             const uint32_t ph = mv | ~(xh | pv);
             const uint32_t mh = pv & xh;
             const int hout = (ph >> 31) ? 1 : ((mh >> 31) ? -1 : 0);
             const uint32_t phs = (ph << 1) | (hin > 0 ? 1u : 0u);
             const uint32_t mhs = (mh << 1) | (hin < 0 ? 1u : 0u);
-            pv = mhs | ~(xv | phs);
-            mv = phs & xv;
-            if (act) st[static_cast<int64_t>(b) * n + (i - 1)] = make_uint4(pv, mv, ph, mh);
-            if (lane == 31 && more) hb[i - 1] = static_cast<int8_t>(hout);
-            out = (code << 2) | (hout + 1);
+            const uint32_t pv2 = mhs | ~(xv | phs), mv2 = phs & xv;
+            if (valid) {
+                pv = pv2;
+                mv = mv2;
+                if (act) st[static_cast<int64_t>(b) * n + (i - 1)] = make_uint4(pv, mv, ph, mh);
+                if (lane == 31 && more) hb[i - 1] = static_cast<int8_t>(hout);
+                out = (code << 2) | (hout + 1);
+            }
         }
         __syncwarp();  // lane 31's carries and the stored columns are read across lanes next
     }

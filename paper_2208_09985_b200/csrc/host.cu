@@ -1332,8 +1332,11 @@ int sg_global_align(const sg_packed_pairs* pairs, int device, sg_results* out) {
         st.dense.ensure(static_cast<size_t>(std::max<int64_t>(pp.scratch_bytes, 4)));
         st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
         // The delta store (16 B per 32 cells) goes in batches of pairs within a
-        // memory budget (SG_EXACT_BUDGET bytes, default 4 GiB; a larger pair runs alone).
-        int64_t budget = int64_t{4} << 30;
+        // memory budget: half the free device memory (at least 4 GiB), or
+        // SG_EXACT_BUDGET bytes; a pair larger than the budget runs alone.
+        size_t free_b = 0, total_b = 0;
+        SG_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        int64_t budget = std::max<int64_t>(int64_t{4} << 30, static_cast<int64_t>(free_b / 2));
         if (const char* e = getenv("SG_EXACT_BUDGET")) budget = std::max<int64_t>(1, atoll(e));
         PinBuf soff, hoff;
         soff.ensure(8 * n1);
