@@ -196,6 +196,7 @@ struct DevState {
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
+    DevBuf q_band, q_full, defer_count, resume_state;  // K1 mixed hand-over (§3.8)
     long long grid = 0, lanes = 0;
 
     void init(int dev) {
@@ -213,7 +214,8 @@ struct DevState {
         for (DevBuf* b : {&seq, &nmask, &text_off, &pat_off, &text_len, &pat_len, &has_n, &order,
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
-                          &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off})
+                          &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
+                          &q_band, &q_full, &defer_count, &resume_state})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
@@ -520,6 +522,7 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split
 struct RunConfig {
     int L, W, O, et, policy, single, k_single;
     bool wide;  // K6 (one warp per pair): windows wider than 128 bits
+    bool band;  // K1b band pass first, full-frame K1 resumes what it defers (§3.8)
     int wcap;   // K6: widest window in columns
 };
 
@@ -549,6 +552,8 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
     r.O = c->O;
     r.et = c->early_termination ? 1 : 0;
     r.policy = c->dent ? 2 : c->sene ? 1 : 0;
+    const char* nb = getenv("SG_NO_BAND");  // experiments / cross-checks: full frame only
+    r.band = !r.wide && sgk::band_eligible(r.W, r.O, r.single) && !(nb && nb[0] == '1');
     return r;
 }
 
@@ -623,7 +628,7 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool str
 // K1 grid for n pairs. Each lane aligns whole pairs one after another, so a
 // batch takes about ceil(n / lanes) pair-times. Use the fewest lanes that keep
 // that number of rounds (fewer warps per SM run each round faster).
-long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
+long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_pass = false) {
     if (rc.wide) {  // K6: one warp per pair, persistent
         const int wpb = sgk::wide_warps_per_block();
         const long long bps = std::max(1, sgk::wide_max_blocks_per_sm());
@@ -633,9 +638,10 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
         warps = std::max(1LL, std::min(warps, (4LL << 30) / per));
         return (warps + wpb - 1) / wpb;
     }
-    int blocks_per_sm = sgk::k1_max_blocks_per_sm(rc.L);
+    int blocks_per_sm = band_pass ? sgk::mixed_max_blocks_per_sm(rc.L) : sgk::k1_max_blocks_per_sm(rc.L);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
-    const int wpb = sgk::k1_warps_per_block(rc.L);
+    // mixed: size by the band warps (they take the fresh pairs)
+    const int wpb = band_pass ? sgk::mixed_band_warps() : sgk::k1_warps_per_block(rc.L);
     const long long max_grid = static_cast<long long>(st.sms) * blocks_per_sm;
     const long long max_lanes = max_grid * wpb * 32;
     const long long rounds = std::max(1LL, (static_cast<long long>(n) + max_lanes - 1) / max_lanes);
@@ -648,6 +654,7 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n) {
 
 // Pairs K1 / K6 work on at once (lanes / warps of the grid).
 int64_t pairs_in_flight(const DevState& st, const RunConfig& rc, int64_t n) {
+    if (rc.band) return k1_grid(st, rc, n, true) * sgk::mixed_band_warps() * 32;
     const long long g = k1_grid(st, rc, n);
     return rc.wide ? g * sgk::wide_warps_per_block() : g * sgk::k1_warps_per_block(rc.L) * 32;
 }
@@ -670,6 +677,14 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     const long long grid = k1_grid(st, rc, n);
     st.grid = grid;
     st.lanes = grid * wpb * (rc.wide ? 1 : 32);  // pairs in flight
+    const long long grid_band = rc.band ? k1_grid(st, rc, n, true) : 0;
+    if (rc.band) {
+        st.lanes = grid_band * sgk::mixed_band_warps() * 32;
+        st.q_band.ensure(4 * (n1 + 32));
+        st.q_full.ensure(4 * (n1 + 32));
+        st.defer_count.ensure(64);
+        st.resume_state.ensure(16 * n1);
+    }
     st.bnd.ensure(rc.wide ? static_cast<size_t>(sgk::wide_warp_words(rc.wcap)) * 4 * grid * wpb
                           : sgk::bnd_scratch_bytes(rc.L, grid * wpb));
     if (!st.bnd_ones.p) {
@@ -679,7 +694,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         SG_CUDA_CHECK(cudaMemsetAsync(st.bnd_ones.p, 0xFF, cb, st.stream));
         SG_CUDA_CHECK(cudaMemsetAsync(st.bnd_zeros.p, 0, cb, st.stream));
     }
-    SG_CUDA_CHECK(cudaMemsetAsync(st.next_pair.p, 0, 4, st.stream));
+    SG_CUDA_CHECK(cudaMemsetAsync(st.next_pair.p, 0, 64, st.stream));
 
     sgk::AlignParams p{};
     p.seq = st.seq.as<uint32_t>();
@@ -728,8 +743,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     if (const char* e = getenv("SG_PHASE_CYCLES")) {
         if (e[0] == '1') {
             static unsigned long long* dbuf = nullptr;
-            if (!dbuf) SG_CUDA_CHECK(cudaMalloc(&dbuf, 64));
-            SG_CUDA_CHECK(cudaMemsetAsync(dbuf, 0, 64, st.stream));
+            if (!dbuf) SG_CUDA_CHECK(cudaMalloc(&dbuf, 256));
+            SG_CUDA_CHECK(cudaMemsetAsync(dbuf, 0, 256, st.stream));
             p.phase_cycles = dbuf;
             g_phase_buf = dbuf;
         }
@@ -737,7 +752,23 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
 
     int launches = 0;
     SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
-    if (n > 0) {
+    if (n > 0 && rc.band) {
+        // K1 mixed: band warps take every pair first; windows the band frame
+        // cannot take move with their pair to the block's full-frame warps and
+        // back (§3.8)
+        p.mixed = 1;
+        p.q_band = st.q_band.as<uint32_t>();
+        p.q_full = st.q_full.as<uint32_t>();
+        p.remaining = st.defer_count.as<unsigned int>();
+        p.resume_state = st.resume_state.as<int32_t>();
+        SG_CUDA_CHECK(cudaMemsetAsync(st.q_band.p, 0, st.q_band.cap, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.q_full.p, 0, st.q_full.cap, st.stream));
+        SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_queue_init(
+            p.q_band, p.q_full, p.remaining, static_cast<int>(n), st.stream)));
+        SG_CUDA_CHECK(static_cast<cudaError_t>(
+            sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
+        launches += 2;
+    } else if (n > 0) {
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             rc.wide ? sgk::launch_wide_align(p, static_cast<int>(grid), st.stream)
                     : sgk::launch_window_align(rc.L, p, static_cast<int>(grid), wpb, st.stream)));
@@ -1288,7 +1319,7 @@ int sg_debug_warp_times(unsigned long long* out, int cap) {
 
 int sg_debug_phase_cycles(unsigned long long* out8) {
     if (!g_phase_buf) return -1;
-    cudaMemcpy(out8, g_phase_buf, 64, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out8, g_phase_buf, 18 * 8, cudaMemcpyDeviceToHost);
     return 0;
 }
 

@@ -355,7 +355,8 @@ template <int L, int R, int C, int MODE, bool DRAIN>
 __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const LaneMem<L>& M,
                                             uint32_t codes4, uint32_t codes4n, int col_top,
                                             uint32_t two, uint32_t one, int g0, bool z0, int n_w,
-                                            const uint32_t* rb, int r0, int p0, int off, int& fr) {
+                                            const uint32_t* rb, int r0, int p0, int off, int& fr,
+                                            bool live) {
     static_assert(R == 4, "groups are aligned to 4-column text-code words");
     constexpr int WB = 32 * L;
     constexpr bool SLOW = MODE == kSlow, CAP = MODE != kOut;
@@ -398,7 +399,8 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
                 pb = M.bnd + (colf >= 0 && colf < n_w ? colf + 4 : WB + 4) * 32 * L;         \
                 px = M.xy + xslot<C>(colf, n_w) * 64;                                        \
             }                                                                                \
-            _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];             \
+            if (live) /* idle lanes: the slots may hold a band-frame window's EQ */     \
+                _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];         \
             if (CAP) {                                                                       \
                 uint2 o;                                                                     \
                 o.x = F.ox | band_word<L>(S.acc[SL][0], mul); /* cleared per window */      \
@@ -476,57 +478,293 @@ __device__ __forceinline__ int dc_chunk(int n_w, bool live, int m_w, int d0, int
         }
         if (mode == kIn)
             sweep_group<L, R, C, kIn, false>(S, F, M, codes4, codes4n, col_top, two, one, g0, z0,
-                                             n_w, rb, r0, p0, off, fr);
+                                             n_w, rb, r0, p0, off, fr, live);
         else if (mode == kOut)
             sweep_group<L, R, C, kOut, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                              z0, n_w, rb, r0, p0, off, fr);
+                                              z0, n_w, rb, r0, p0, off, fr, live);
         else
             sweep_group<L, R, C, kSlow, false>(S, F, M, codes4, codes4n, col_top, two, one, g0,
-                                               z0, n_w, rb, r0, p0, off, fr);
+                                               z0, n_w, rb, r0, p0, off, fr, live);
         codes4 = codes4n;
     }
     // drain: rows 1..R-1 finish (row 0 has just left column 0)
     if (!top_bit<L, R>(S, 0, r0, p0)) fr = 0;
     sweep_group<L, R, C, kSlow, true>(S, F, M, codes4, codes4, -1, two, one,
-                                      n_w - S0 - d0 + tsteps, z0, n_w, rb, r0, p0, off, fr);
+                                      n_w - S0 - d0 + tsteps, z0, n_w, rb, r0, p0, off, fr, live);
+    return fr;
+}
+
+// ---------------------------------------------------------- band-frame DC (K1b)
+//
+// DESIGN.md §3.8. Rows are kept in DIAGONAL coordinates, one 32-bit word per
+// row: bit k of a row at column i is cell (i, j = i + e_lo + k), complemented
+// (bit = 1 <=> D(i, j) <= d). With e_lo = floor(d0/2) - 16 (d0 = m_w - n_w)
+// the band holds every cell of every path of cost <= 30 from (0, 0) to
+// (n_w, m_w): leaving it costs at least 31. Cells outside read as "D > d"
+// (zeros shifted in), so rows 0..30 give D(0, 0) and every traceback decision
+// exactly (DESIGN.md §3.8 has the argument). The cell update (dp.cpp:187-211 in
+// these coordinates, C = ~R):
+//   C[i][d] = (C[i+1][d] & EQ_i) | C[i+1][d-1] | (C[i+1][d-1] << 1) | (C[i][d-1] >> 1)
+// (match, substitution, deletion, insertion). EQ_i bit k = [t_i == p_j], zero
+// for j >= m_w, so the end-of-pattern column j = m_w is an ordinary band cell
+// (D(i, m_w) = n_w - i) and there are no boundary bits. Traceback events:
+//   X |= C[i+1][d] & ~C[i][d]          (D(i+1, j+1) < D(i, j))
+//   Y |= (C[i+1][d] << 1) & ~C[i][d]   (D(i+1, j) < D(i, j))
+// A cell costs 2 LOP3 + 2 FMA-pipe shifts (x * 2, mul.hi(x, 2^31) = x >> 1),
+// plus 2 LOP3 where events are kept.
+namespace band {
+constexpr int R = 4;
+constexpr int WMAX = 64;              // widest band-mode window (columns)
+constexpr int CMAX = 40;              // traceback-event columns (W - O <= 40)
+constexpr int kLastRow = 30;          // rows 0..30 are exact
+constexpr int WARPS = 6;              // band warps per block (one block per SM) ...
+constexpr int FWARPS = 1;             // ... plus a full-frame warp (K1 mixed)
+constexpr int kBackRow = 24;          // a full-frame warp hands a pair back after D(0,0) <= 24
+// per-warp shared memory, in 32-bit words:
+//   eqp [WMAX + 4][32] uint2  (EQ_i, parked row) of column i at slot i + 4
+//   xy  [CMAX + 1][32] uint2  events X / Y; column C (runtime) is the dummy
+//   sq  packed text / pattern / N words of the window (traceback), as K1<2>
+__host__ __device__ constexpr int eqp_words() { return (WMAX + 4) * 64; }
+__host__ __device__ constexpr int xy_words() { return (CMAX + 1) * 64; }
+}  // namespace band
+
+struct BandState {
+    uint32_t v[4];       // row r's latest value
+    uint32_t dg[4];      // row r-1's value at row r's column + 1 (row 0: parked row)
+    uint32_t dgs[4];     // dg << 1
+    uint32_t eq[4];      // EQ ring: slot s & 3 = the column row 0 entered at step s
+    uint32_t acc[4][2];  // X / Y ring, same slots
+};
+
+__device__ __forceinline__ uint32_t fma_shl(uint32_t x, uint32_t two) {  // x * two (IMAD)
+    uint32_t r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(two));
+    return r;
+}
+__device__ __forceinline__ uint32_t fma_shr(uint32_t x, uint32_t hmul) {  // x * 2^31 >> 32 (IMAD.HI)
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(hmul));
+    return r;
+}
+
+// Row r's cell at step U (static). north: row r-1's value at this column.
+// STD: the standard frame (bit j = cell (i, j), patterns of <= 31 bases, §3.8):
+//   C[i][d] = ((C[i+1][d] >> 1) & EQ_i) | (C[i+1][d-1] >> 1) | C[i+1][d-1] | (C[i][d-1] >> 1)
+// X = (C[i+1][d] >> 1) & ~C, Y = C[i+1][d] & ~C; the same data flow with es = east >> 1.
+template <int U, int r, bool CAP, bool STD>
+__device__ __forceinline__ void band_cell(BandState& S, uint32_t north, uint32_t two,
+                                          uint32_t hmul) {
+    constexpr int SL = (U - r) & 3;
+    const uint32_t east = S.v[r];
+    const uint32_t ns = fma_shr(north, hmul);
+    const uint32_t es = STD ? fma_shr(east, hmul) : fma_shl(east, two);
+    const uint32_t mt = STD ? es : east;  // the match neighbour (i+1, j+1)
+    const uint32_t dl = STD ? east : es;  // the deletion neighbour (i+1, j)
+    const uint32_t c = (mt & S.eq[SL]) | S.dg[r] | S.dgs[r] | ns;
+    if (CAP) {
+        if (r == 0) {
+            S.acc[SL][0] = mt & ~c;
+            S.acc[SL][1] = dl & ~c;
+        } else {
+            S.acc[SL][0] |= mt & ~c;
+            S.acc[SL][1] |= dl & ~c;
+        }
+    }
+    if (r + 1 < 4) {
+        S.dg[r + 1 < 4 ? r + 1 : 0] = east;
+        S.dgs[r + 1 < 4 ? r + 1 : 0] = es;
+    }
+    S.v[r] = c;
+}
+
+enum { kBFill = 0, kBOut = 1, kBIn = 2, kBMix = 3, kBDrain = 4 };
+
+// Lane views: eqp + lane (uint2 stride 32 per column slot), xy + lane.
+struct BandMem {
+    uint2* eqp;  // slot(col) = col + 4
+    uint2* xy;   // column c at xy[c * 32]
+};
+
+// One group of 4 steps. Row 0 works on columns col_top .. col_top - 3; row r
+// lags r columns. MODE: kBFill (rows r <= U start at column W-1), kBDrain
+// (rows r > U finish at column 0), kBOut (no event columns), kBIn (every
+// finished column keeps events), kBMix (stores of columns >= C go to the dummy).
+template <int MODE, int U, bool STD>
+__device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const BandMem& M,
+                                          int col_top, int C, uint32_t keep, uint32_t two,
+                                          uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
+                                          uint32_t one_l, bool live) {
+    constexpr bool CAP = MODE != kBOut;
+    constexpr bool ROW3 = (MODE == kBFill ? U == 3 : true) && (MODE != kBDrain || U < 3);
+    constexpr bool STORE_EV = CAP && ROW3;
+    const int c3 = col_top - U + 3;  // the column row 3 finishes at this step
+    uint2* px = M.xy + (MODE == kBIn ? c3 : (c3 < C ? c3 : C)) * 32;
+    uint2 old = make_uint2(0u, 0u);
+    if (STORE_EV) old = *px;
+    const uint2 f = F[U];
+    if (MODE != kBDrain) F[U] = M.eqp[(col_top - U - 4 + 4) * 32];  // next group's column
+    // rows 3..1 (descending: a row reads its upper row's value before it updates)
+#define SG_BCELL(r)                                                                   \
+    if ((MODE == kBFill && (r) <= U) || (MODE == kBDrain && (r) > U) ||               \
+        (MODE != kBFill && MODE != kBDrain))                                          \
+        band_cell<U, (r), CAP, STD>(S, S.v[(r) - 1], two, hmul);
+    SG_BCELL(3) SG_BCELL(2) SG_BCELL(1)
+#undef SG_BCELL
+    if (MODE != kBDrain) {  // row 0: north = parked row of this column, masked for idle lanes
+        S.eq[U] = f.x;
+        band_cell<U, 0, CAP, STD>(S, f.y, two, hmul_l);
+        S.dg[0] = fma_shl(f.y, one_l);
+        S.dgs[0] = STD ? fma_shr(f.y, hmul_l) : fma_shl(f.y, two_l);
+    }
+    if (ROW3) {
+        // park row 3 (idle lanes do not: in a full-frame warp the slot may be
+        // another frame's parked row)
+        if (live) reinterpret_cast<uint32_t*>(M.eqp + (c3 + 4) * 32)[1] = S.v[3];
+        if (STORE_EV) {
+            constexpr int SL3 = (U + 1) & 3;
+            uint2 o;
+            o.x = (old.x & keep) | S.acc[SL3][0];
+            o.y = (old.y & keep) | S.acc[SL3][1];
+            *px = o;
+        }
+    }
+}
+
+// One group of 4 steps. Row 0 works on columns col_top .. col_top - 3; row r
+// lags r columns. MODE: kBFill (rows r <= U start at column W-1), kBDrain
+// (rows r > U finish at column 0), kBOut (no event columns), kBIn (every
+// finished column keeps events), kBMix (stores of columns >= C go to the dummy).
+template <int MODE, bool STD>
+__device__ __forceinline__ void band_group(BandState& S, uint2 (&F)[4], const BandMem& M,
+                                           int col_top, int C, uint32_t keep, uint32_t two,
+                                           uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
+                                           uint32_t one_l, bool live) {
+    band_step<MODE, 0, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 1, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 2, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 3, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+}
+
+// init column (i = n_w) of row d: bits k in [K0 - d, K0] (D(n, j) = m - j <= d)
+__device__ __forceinline__ uint32_t band_init(int d, int K0) {
+    if (d < 0) return 0u;
+    const int lo = max(K0 - d, 0);
+    return (0xFFFFFFFFu >> (31 - K0)) & (0xFFFFFFFFu << lo);
+}
+
+// One chunk of rows d0..d0+3 over the W columns of a band window. Returns the
+// first row r with D(0, 0) <= d0 + r, or -1. Idle lanes (live = false) run on
+// all-zero rows: they keep their stored events and park zeros.
+template <bool STD>
+__device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K0, int k00,
+                                          const BandMem& M, uint32_t two, uint32_t hmul) {
+    const uint32_t lv = live ? ~0u : 0u;
+    // a live lane's first chunk of a window overwrites the events; otherwise OR
+    const uint32_t keep = live && d0 == 0 ? 0u : ~0u;
+    BandState S;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        S.v[r] = band_init(d0 + r, K0) & lv;
+        S.dg[r] = band_init(d0 + r - 1, K0) & lv;
+        S.dgs[r] = STD ? S.dg[r] >> 1 : S.dg[r] << 1;
+        S.eq[r] = 0u;
+        S.acc[r][0] = S.acc[r][1] = 0u;
+    }
+    const uint32_t two_l = two & lv, hmul_l = hmul & lv, one_l = (two >> 1) & lv;
+    uint2 F[4];
+#pragma unroll
+    for (int U = 0; U < 4; ++U) F[U] = M.eqp[(W - 1 - U + 4) * 32];
+    band_group<kBFill, STD>(S, F, M, W - 1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    for (int col_top = W - 5; col_top >= 3; col_top -= 4) {
+        if (col_top - 3 >= C)
+            band_group<kBOut, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+        else if (col_top + 3 < C)
+            band_group<kBIn, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+        else
+            band_group<kBMix, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    }
+    band_group<kBDrain, STD>(S, F, M, -1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    int fr = -1;
+#pragma unroll
+    for (int r = 3; r >= 0; --r)
+        if ((S.v[r] >> k00) & 1u) fr = r;
     return fr;
 }
 
 // ------------------------------------------------------------------ K1
 
-template <int L>
-__global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
-    k1_window_align(const AlignParams P) {
+// Shared memory words of one K1 warp (BAND: the band-frame layout, §3.8).
+template <int L, bool BAND> __host__ __device__ constexpr int k1_warp_words() {
+    return BAND ? band::eqp_words() + band::xy_words() + sq_words<L>() : warp_smem_words<L>();
+}
+// Hand-over queues between band and full-frame warps (K1 mixed, §3.8): a ring
+// of pair ids, q[0] = head, q[1] = tail, slots q[32 + k % cap] hold pair + 1
+// (0 = empty). The pair's state is written before the slot is published.
+__device__ __forceinline__ void q_push(uint32_t* q, int cap, int pair) {
+    __threadfence();
+    const unsigned t = atomicAdd(q + 1, 1u);
+    uint32_t* slot = q + 32 + t % static_cast<unsigned>(cap);
+    while (atomicCAS(slot, 0u, static_cast<uint32_t>(pair) + 1u) != 0u) __nanosleep(200);
+}
+__device__ __forceinline__ int q_pop(uint32_t* q, int cap) {
+    const unsigned h = *reinterpret_cast<volatile unsigned*>(q);
+    const unsigned t = *reinterpret_cast<volatile unsigned*>(q + 1);
+    if (static_cast<int>(t - h) <= 0) return -1;
+    if (atomicCAS(q, h, h + 1u) != h) return -1;  // another lane took it: retry later
+    uint32_t* slot = q + 32 + h % static_cast<unsigned>(cap);
+    uint32_t v;
+    while ((v = atomicExch(slot, 0u)) == 0u) __nanosleep(200);  // reserved, not yet written
+    __threadfence();
+    return static_cast<int>(v) - 1;
+}
+
+// The K1 window loop of one warp. BAND = true: the band frame (K1b) — windows
+// it cannot take (final windows, n_w < W, |m_w - n_w| > 30, D(0, 0) > 30) go
+// with the pair to a full-frame warp (P.mixed); a full-frame warp hands the
+// pair back once its next window is a band window again.
+template <int L, bool BAND>
+__device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wbase,
+                                        const long long gwarp, uint32_t* const bnd_smem,
+                                        uint32_t* const eqp_smem) {
+    static_assert(!BAND || L == 2, "the band pass stages sequences as K1<2>");
     constexpr int R = KCfg<L>::R, C = KCfg<L>::C, WB = 32 * L, NW = 2 * L;
-    extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    uint32_t* const wbase = smem + wib * warp_smem_words<L>();
     uint64_t* const txt = reinterpret_cast<uint64_t*>(wbase);   // [WB/8][32]
-    uint32_t* const xy = wbase + txt_words<L>();                 // [C+1][32][2]
+    uint32_t* const xy = BAND ? wbase + band::eqp_words()       // band: [CMAX+1][32][2]
+                              : wbase + txt_words<L>();         // [C+1][32][2]
     uint32_t* const pmv = xy + xy_words<L>();                    // [5][32][L]
-    uint32_t* const sq = pmv + pm_words<L>();                    // [6L+4][32]
+    uint32_t* const sq = BAND ? xy + band::xy_words() : pmv + pm_words<L>();  // [6L+4][32]
+    // band warps: (EQ, parked row) at the start of the warp's memory; full-frame
+    // warps of the mixed kernel: STD windows use the parked-row region
+    const BandMem bmem{reinterpret_cast<uint2*>(BAND ? wbase : eqp_smem) + lane,
+                       reinterpret_cast<uint2*>(xy) + lane};
     constexpr int PFW = pf_words<L>();
     uint32_t* const sq_t = sq;                                   // text staging (PFW words)
     uint32_t* const sq_p = sq + PFW * 32;                        // pattern staging (PFW)
     uint32_t* const sq_tn = sq + 2 * PFW * 32;                   // text N words (L+1)
     uint32_t* const sq_pn = sq + (2 * PFW + L + 1) * 32;         // pattern N words (L+1)
-    const long long gwarp = static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib;
-    uint32_t* const bnd = P.bnd + gwarp * (WB + 5) * 32 * L;    // [WB+5][32][L]
+    // parked rows [WB+5][32][L]: in shared memory for the mixed kernel's full-frame warp
+    uint32_t* const bnd = bnd_smem ? bnd_smem : P.bnd + gwarp * (WB + 5) * 32 * L;
     const uint32_t two = static_cast<uint32_t>(P.two), one = two >> 1;
     const LaneMem<L> lmem{bnd + lane * L, P.bnd_ones + lane * L, P.bnd_zeros + lane * L,
                           xy + lane * 2, pmv + lane * L,
                           reinterpret_cast<const uint32_t*>(txt) + lane};
 
+    if (!BAND) {
 #pragma unroll
-    for (int l = 0; l < L; ++l) pmv[(4 * 32 + lane) * L + l] = ~0u;  // non-ACGT text
+        for (int l = 0; l < L; ++l) pmv[(4 * 32 + lane) * L + l] = ~0u;  // non-ACGT text
 #pragma unroll
-    for (int b = 0; b <= WB / 4; ++b)  // idle lanes and the column -1 pad: code 4
-        reinterpret_cast<uint32_t*>(txt)[b * 32 + lane] = 0x04040404u;
+        for (int b = 0; b <= WB / 4; ++b)  // idle lanes and the column -1 pad: code 4
+            reinterpret_cast<uint32_t*>(txt)[b * 32 + lane] = 0x04040404u;
+    }
 
     const int W = P.W;
     const int step_limit = W - P.O;
     const int K = P.single ? P.k_single : W;  // edit budget: rows 0..K
+    // band pass: traceback-event columns, last exact row, shift multipliers
+    const int cmax = BAND ? step_limit : C;
+    const int band_last = min(K, band::kLastRow);
+    const uint32_t hmul = two << 30;  // 2^31 at run time: mul.hi(x, hmul) = x >> 1
 
     // ---- lane state ----
     int pair = -1;
@@ -538,6 +776,11 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
     int d0 = 0, found_d = -1, expect_d = -1;
     int dist = 0, nwin = 0, status = 0;
     int window_cap = 0;
+    int e_lo = 0, K0 = 0;  // band window: bit k <-> j = i + e_lo + k; (n_w, m_w) at bit K0
+    int pass_win = 0;      // windows this warp completed for the pair (hand-back after one)
+    int last_d = 0;        // D(0, 0) of the last window
+    bool defer_now = false;
+    bool std_win = false;  // full-frame warp, mixed: the window runs in the STD frame (m_w <= 31)
     // Sequence staging: sq_t / sq_p hold PFW packed words from word st_tw / st_pw;
     // the segment's text / pattern start at base t_sh / p_sh inside them. The
     // words of the region the next window can start in are prefetched into
@@ -637,6 +880,96 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             load_bits<L + 1>(P.nmask, pbase + poff, pn);
             load_bits<L + 1>(P.nmask, tbase + toff, tn);
         }
+        if (!BAND && std_win) {
+            // (§3.8) STD frame: EQ_i = plane t_i of the pattern, bits j < m_w <= 31;
+            // the planes go to this lane's pattern-mask slots, the parked row
+            // starts as row -1 (zeros)
+            const uint32_t lo = compress_stride<2>(pw[0] & 0x55555555u) |
+                                (compress_stride<2>(pw[1] & 0x55555555u) << 16);
+            const uint32_t hi = compress_stride<2>((pw[0] >> 1) & 0x55555555u) |
+                                (compress_stride<2>((pw[1] >> 1) & 0x55555555u) << 16);
+            const uint32_t valid = ((1u << m_w) - 1u) & ~pn[0];
+            uint32_t* const pl = pmv + lane * L;  // [5][32][L] words, limb 0 used
+            pl[0 * 32 * L] = ~lo & ~hi & valid;
+            pl[1 * 32 * L] = lo & ~hi & valid;
+            pl[2 * 32 * L] = ~lo & hi & valid;
+            pl[3 * 32 * L] = lo & hi & valid;  // (code 4's all-ones full-frame mask stays)
+            for (int k = 0; 16 * k < n_w; ++k) {
+                const int bt = t_sh + 16 * k;
+                const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
+                                                       sq_t[((bt >> 4) + 1) * 32 + lane],
+                                                       2 * (bt & 15));
+                const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int code = static_cast<int>((tword >> (2 * u)) & 3u);
+                    uint32_t e = pl[code * 32 * L];
+                    if (hasn && ((tnw >> u) & 1u)) e = 0u;  // non-ACGT text matches nothing
+                    bmem.eqp[(16 * k + u + 4) * 32] = make_uint2(e, 0u);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k <= L; ++k) {
+                sq_tn[k * 32 + lane] = tn[k];
+                sq_pn[k * 32 + lane] = pn[k];
+            }
+            return;
+        }
+        if constexpr (BAND) {
+            // (§3.8) code planes of the pattern over j in [-32, 96) as (word w, word
+            // w + 1) pairs, w = 0..2, one uint2 per (code, w) in this lane's event
+            // columns 0..14 (dead until the window's first chunk overwrites them);
+            // code 4 (non-ACGT text) matches nothing
+            uint32_t plo[2], phi[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                plo[h] = compress_stride<2>(pw[2 * h] & 0x55555555u) |
+                         (compress_stride<2>(pw[2 * h + 1] & 0x55555555u) << 16);
+                phi[h] = compress_stride<2>((pw[2 * h] >> 1) & 0x55555555u) |
+                         (compress_stride<2>((pw[2 * h + 1] >> 1) & 0x55555555u) << 16);
+            }
+            uint2* const lut = bmem.xy;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                uint32_t q[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int vb = min(max(m_w - 32 * h, 0), 32);
+                    const uint32_t valid = (vb == 32 ? ~0u : ((1u << vb) - 1u)) & ~pn[h];
+                    const uint32_t lo = plo[h], hi = phi[h];
+                    const uint32_t e = c == 0 ? ~lo & ~hi : c == 1 ? lo & ~hi
+                                       : c == 2 ? ~lo & hi : c == 3 ? lo & hi : 0u;
+                    q[h + 1] = e & valid;  // j >= m_w and pattern N: no match
+                }
+#pragma unroll
+                for (int w = 0; w < 3; ++w) lut[(3 * c + w) * 32] = make_uint2(q[w], q[w + 1]);
+            }
+            // EQ_i of every column: bits j in [i + e_lo, i + e_lo + 32) of plane t_i;
+            // the parked row starts as row -1 (all zeros)
+            const int ob = e_lo + 32;  // bit offset of column 0's window from j = -32
+            for (int k = 0; 16 * k < n_w; ++k) {
+                const int bt = t_sh + 16 * k;
+                const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
+                                                       sq_t[((bt >> 4) + 1) * 32 + lane],
+                                                       2 * (bt & 15));
+                const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int i = 16 * k + u;
+                    int code = static_cast<int>((tword >> (2 * u)) & 3u);
+                    if (hasn && ((tnw >> u) & 1u)) code = 4;
+                    const int o = ob + i;
+                    const uint2 pr = lut[(3 * code + (o >> 5)) * 32];
+                    bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, o & 31), 0u);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k <= L; ++k) {
+                sq_tn[k * 32 + lane] = tn[k];
+                sq_pn[k * 32 + lane] = pn[k];
+            }
+            return;
+        }
         uint32_t pwl[NW], pnl[L];
 #pragma unroll
         for (int k = 0; k < NW; ++k) pwl[k] = pw[k];
@@ -682,27 +1015,63 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
     };
 
     // Geometry of the next logical window of the current pair
-    // (aligner.cpp:44-64). Returns false when the pair is complete (residues
-    // appended).
-    auto next_window = [&]() -> bool {
+    // (aligner.cpp:44-64). Returns 0 when the pair is complete (residues
+    // appended), 1 for a window, 2 (band pass) when the window is not a band
+    // window: the pair goes to the full-frame resume pass from here.
+    auto next_window = [&]() -> int {
         const int n_rem = n_tot - toff, m_rem = m_tot - poff;
         if (n_rem == 0 || m_rem == 0) {
             if (n_rem + m_rem > 0) {  // aligner.cpp:48-57
                 emit(n_rem == 0 ? 2 : 3, n_rem + m_rem);
                 dist += n_rem + m_rem;
             }
-            return false;
+            return 0;
         }
         // single-window mode (aligner.cpp:87-112): the whole pair is one final window
         const bool fin = P.single || (n_rem <= W && m_rem <= W);
         n_w = P.single ? n_rem : min(W, n_rem);
         m_w = P.single ? m_rem : min(W, m_rem);
+        {
+            const int dl = m_w - n_w;
+            const bool band_ok = !fin && n_w == W && dl <= band::kLastRow && dl >= -band::kLastRow;
+            if (BAND) {
+                if (!band_ok) return 2;
+                e_lo = (dl >> 1) - 16;
+                K0 = dl - e_lo;
+            } else if (P.mixed && band_ok && pass_win > 0 && last_d <= band::kBackRow) {
+                return 2;  // back on track: the band frame takes the pair again
+            }
+            std_win = !BAND && bnd_smem != nullptr && !fin && n_w == W && m_w <= 31;
+        }
         limit = fin ? -1 : step_limit;
         first_seg = true;
         d0 = 0;
         found_d = -1;
         expect_d = -1;
-        return true;
+        return 1;
+    };
+
+    // Hand the pair to the next pass (the other frame) before its current window.
+    auto defer_pair = [&]() {
+        P.distance[pair] = dist;
+        P.windows[pair] = nwin;
+        P.status[pair] = 0;
+        P.out_bytes[pair] = out_bytes;
+        if (P.counters) {
+            uint64_t* c = P.counters + 7ll * pair;
+            c[0] = c_stored;
+            c[1] = c_writes;
+            c[2] = c_reads;
+            c[3] = c_rows;
+            c[4] = c_cells;
+            c[6] = c_bequiv;
+        }
+        int32_t* rs = P.resume_state + 4ll * pair;
+        rs[0] = toff;
+        rs[1] = poff;
+        rs[2] = (cur_op & 0xFF) | (cur_len << 8);
+        rs[3] = static_cast<int32_t>(acc);
+        q_push(BAND ? P.q_full : P.q_band, P.n_pairs, pair);
     };
 
     auto finish_pair = [&]() {
@@ -722,17 +1091,32 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
             c[6] = c_bequiv;
         }
+        if (P.mixed) atomicSub(P.remaining, 1u);
     };
 
     // Claim the next pair for the calling (possibly divergent) lanes.
     auto fetch = [&]() {
-        const unsigned active = __activemask();
-        const int leader = __ffs(active) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(P.next_pair, static_cast<unsigned>(__popc(active)));
-        base = __shfl_sync(active, base, leader);
-        const int q = static_cast<int>(base + __popc(active & ((1u << lane) - 1u)));
-        pair = q < P.n_pairs ? (P.order ? P.order[q] : q) : -1;
+        pair = -1;
+        bool restore = false;
+        if (P.mixed) {  // a pair handed over by the other frame first
+            pair = q_pop(BAND ? P.q_band : P.q_full, P.n_pairs);
+            restore = pair >= 0;
+        }
+        if (BAND || !P.mixed) {  // fresh pairs (warp-aggregated claim)
+            const bool want = pair < 0 &&
+                (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.next_pair) <
+                                 static_cast<unsigned>(P.n_pairs));
+            const unsigned active = __activemask();
+            const unsigned wm = __ballot_sync(active, want);
+            if (want) {
+                const int leader = __ffs(wm) - 1;
+                unsigned base = 0;
+                if (lane == leader) base = atomicAdd(P.next_pair, static_cast<unsigned>(__popc(wm)));
+                base = __shfl_sync(wm, base, leader);
+                const int q = static_cast<int>(base + __popc(wm & ((1u << lane) - 1u)));
+                pair = q < P.n_pairs ? (P.order ? P.order[q] : q) : -1;
+            }
+        }
         if (pair < 0) return;
         n_tot = P.text_len[pair];
         m_tot = P.pat_len[pair];
@@ -756,6 +1140,30 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         acc = 0;
         acc_n = 0;
         c_stored = c_writes = c_reads = c_rows = c_cells = c_bequiv = 0;
+        pass_win = 0;
+        if (restore) {  // continue where the other frame stopped (state written before the push)
+            const int4 rs = __ldcg(reinterpret_cast<const int4*>(P.resume_state + 4ll * pair));
+            toff = rs.x;
+            poff = rs.y;
+            cur_op = (rs.z & 0xFF) == 0xFF ? -1 : (rs.z & 0xFF);
+            cur_len = rs.z >> 8;
+            acc = static_cast<uint32_t>(rs.w);
+            dist = __ldcg(P.distance + pair);
+            nwin = __ldcg(P.windows + pair);
+            out_bytes = __ldcg(P.out_bytes + pair);
+            acc_n = out_bytes & 3;
+            outw += out_bytes >> 2;
+            if (P.counters) {
+                const unsigned long long* c =
+                    reinterpret_cast<const unsigned long long*>(P.counters + 7ll * pair);
+                c_stored = __ldcg(c + 0);
+                c_writes = __ldcg(c + 1);
+                c_reads = __ldcg(c + 2);
+                c_rows = __ldcg(c + 3);
+                c_cells = __ldcg(c + 4);
+                c_bequiv = __ldcg(c + 6);
+            }
+        }
     };
 
     // Matching bases from (i, j) on (0..16; 0 at a mismatch or a non-ACGT base).
@@ -781,26 +1189,36 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         return __clz(__brev(x)) >> 1;  // 16 when all 16 bases match
     };
 
+    const long long dwarp = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (P.warp_times && lane == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        P.warp_times[gwarp * 3] = t;
+        P.warp_times[dwarp * 3] = t;
     }
+    unsigned long long last_busy = 0;
     bool need_pair = true, need_window = false, need_load = false;
     unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0, ph_act = 0, ph_trips = 0,
-                       ph_steps = 0, ph_tbn = 0;
+                       ph_steps = 0, ph_tbn = 0, ph_idle = 0;
     for (;;) {
         const long long ck0 = clock64();
         // ---------------------------------------------- per-lane setup
         while (need_pair || need_window) {
             if (need_pair) {
                 fetch();
+                if (pair < 0) {
+                    need_pair = P.mixed != 0;  // mixed: retry (work may be handed over)
+                    break;
+                }
                 need_pair = false;
-                if (pair < 0) break;
                 need_window = true;
             }
-            if (status == 0 && next_window()) {
+            const int nw = status == 0 ? next_window() : 0;
+            if (nw == 1) {
                 need_load = true;
+            } else if (nw == 2) {
+                defer_pair();
+                pair = -1;
+                need_pair = true;
             } else {
                 finish_pair();
                 pair = -1;
@@ -813,7 +1231,16 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             need_load = false;
         }
         const bool in_dc = pair >= 0;
-        if (!__any_sync(kFull, in_dc)) break;
+        if (!__any_sync(kFull, in_dc)) {
+            if (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
+            if (P.warp_times && lane == 0 && last_busy == 0) {  // diagnostics: first idle moment
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_busy));
+            }
+            // pairs are still in flight: one may be handed to this warp
+            __nanosleep(BAND ? 2000 : 8000);
+            ph_idle += clock64() - ck0;
+            continue;
+        }
         __syncwarp();
         const long long ck1 = clock64();
 
@@ -824,8 +1251,37 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         for (int sub = 0; sub < kSubChunks; ++sub) {
             const bool act = in_dc && !solved;
             if (sub > 0 && !__any_sync(kFull, act)) break;
-            const int n_max = warp_max(act ? n_w : 0);
-            const int fr = dc_chunk<L, R, C>(act ? n_w : 0, act, m_w, d0, n_max, two, one, lmem);
+            if constexpr (BAND) {
+                const int fr = band_chunk<false>(act, d0, W, cmax, K0, -e_lo, bmem, two, hmul);
+                ++ph_it;
+                ph_act += __popc(__ballot_sync(kFull, act));
+                if (act) {
+                    if (found_d < 0 && fr >= 0) found_d = d0 + fr;
+                    // D(0, 0) is exact up to band_last; beyond it the window goes
+                    // to the full frame (resume pass)
+                    solved = found_d >= 0 || d0 + R > band_last;
+                    if (solved && (found_d < 0 || found_d > band_last)) defer_now = true;
+                    if (!solved) d0 += R;
+                }
+                continue;
+            }
+            int fr = -1;
+            if (!BAND && bnd_smem) {  // mixed full-frame warp: STD windows first
+                const bool act_std = act && std_win;
+                if (__any_sync(kFull, act_std)) {
+                    const int f = band_chunk<true>(act_std, d0, W, C, m_w, 0, bmem, two, hmul);
+                    if (act_std) fr = f;
+                    ++ph_it;
+                    ph_act += __popc(__ballot_sync(kFull, act_std));
+                }
+            }
+            const bool act_full = act && !std_win;
+            if (__any_sync(kFull, act_full)) {
+                const int n_max = warp_max(act_full ? n_w : 0);
+                const int f = dc_chunk<L, R, C>(act_full ? n_w : 0, act_full, m_w, act_full ? d0 : 0,
+                                                n_max, two, one, lmem);
+                if (act_full) fr = f;
+            }
             ++ph_it;
             ph_act += __popc(__ballot_sync(kFull, act));
             if (act) {
@@ -842,11 +1298,17 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
 
         // ------------------------------------------------ TB + advance
         int tb_trip = 0;
-        if (in_dc && solved) {
+        if (BAND && in_dc && solved && defer_now) {
+            defer_now = false;
+            defer_pair();
+            pair = -1;
+            need_pair = true;
+        } else if (in_dc && solved) {
             // single window with D(0, 0) > k: not found (batch.cpp:57-62)
             const bool not_found = P.single && found_d < 0;
             if (found_d < 0 && !not_found) status = kStInternal | kDetNoStep;  // aligner.cpp:69-70
             if (first_seg) {
+                last_d = found_d;
                 // reference counters for this logical window (dp.cpp:23-37,58-75,225-228)
                 const int rows_ref = P.et && found_d >= 0 ? found_d + 1 : K + 1;
                 int pol = P.policy;
@@ -868,6 +1330,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
             if (not_found) {
                 dist = -1;
                 ++nwin;
+                ++pass_win;
                 toff = n_tot;
                 poff = m_tot;
                 need_window = true;
@@ -899,9 +1362,9 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                 ++ph_steps;
                 ++tb_trip;
                 int rem = lim - steps;
-                if (rem == 0 || i == n_w || j == m_w || i >= C) break;
+                if (rem == 0 || i == n_w || j == m_w || i >= cmax) break;
                 const int run = match_run(i, j);
-                const int k = min(min(run, rem), min(min(n_w - i, m_w - j), C - i));
+                const int k = min(min(run, rem), min(min(n_w - i, m_w - j), cmax - i));
                 if (k > 0) {
                     reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
                     i += k;
@@ -910,13 +1373,23 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                     rem -= k;
                     emit_short(0, k);
                 }
-                if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w || i >= C) continue;
+                if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w || i >= cmax) continue;
                 // the edit at the mismatch (i, j)
                 const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
-                const unsigned q = static_cast<unsigned>(j + off);
-                const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
-                if (static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
-                const uint32_t bit = 0x80000000u >> ((32 / L) * (q % L) + dp);
+                uint32_t bit;
+                if constexpr (BAND) {  // diagonal band: cell (i, j) at bit j - i - e_lo
+                    const int kb = j - i - e_lo;
+                    if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
+                        status = kStInternal | kDetSegment;
+                        break;
+                    }
+                    bit = 1u << kb;
+                } else {
+                    const unsigned q = static_cast<unsigned>(j + off);
+                    const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
+                    if (!std_win && static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
+                    bit = std_win ? 1u << j : 0x80000000u >> ((32 / L) * (q % L) + dp);
+                }
                 const int op = ev.x & bit ? 1 : (ev.y & bit ? 3 : 2);
                 if (d == 0) status = kStInternal | kDetNoStep;
                 reads += d == 0 ? 1u : 3u;
@@ -951,6 +1424,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                 }
             }
             if (!P.single) c_reads += reads;  // single window: counted before TB (aligner.cpp:98-99)
+            if (BAND && cont) status = kStInternal | kDetSegment;  // non-final: W - O <= cmax
             if (cont && status == 0) {
                 // the window continues on the suffix t[i:n_w) x p[j:m_w)
                 toff += i;
@@ -968,6 +1442,7 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
                 toff += i;
                 poff += j;
                 ++nwin;
+                ++pass_win;
                 if (nwin > window_cap) status = kStInternal | kDetWatchdog;
                 need_window = true;
             }
@@ -981,22 +1456,66 @@ __global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
         unsigned long long t, smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned*>(&smid)));
-        P.warp_times[gwarp * 3 + 1] = t;
-        P.warp_times[gwarp * 3 + 2] = smid & 0xFFFFFFFFull;
+        P.warp_times[dwarp * 3 + 1] = last_busy ? last_busy : t;
+        P.warp_times[dwarp * 3 + 2] = smid & 0xFFFFFFFFull;
     }
     if (P.phase_cycles) {
         ph_steps = __reduce_add_sync(kFull, static_cast<unsigned>(ph_steps));
         ph_tbn = __reduce_add_sync(kFull, static_cast<unsigned>(ph_tbn));
-        if (lane == 0) {
-            atomicAdd(P.phase_cycles + 0, ph_setup);
-            atomicAdd(P.phase_cycles + 1, ph_dc);
-            atomicAdd(P.phase_cycles + 2, ph_tb);
-            atomicAdd(P.phase_cycles + 3, ph_it);
-            atomicAdd(P.phase_cycles + 4, ph_act);
-            atomicAdd(P.phase_cycles + 5, ph_trips);
-            atomicAdd(P.phase_cycles + 6, ph_steps);
-            atomicAdd(P.phase_cycles + 7, ph_tbn);
+        if (lane == 0) {  // band warps [0, 9), full-frame warps [9, 18)
+            unsigned long long* pc = P.phase_cycles + (BAND ? 0 : 9);
+            atomicAdd(pc + 0, ph_setup);
+            atomicAdd(pc + 1, ph_dc);
+            atomicAdd(pc + 2, ph_tb);
+            atomicAdd(pc + 3, ph_it);
+            atomicAdd(pc + 4, ph_act);
+            atomicAdd(pc + 5, ph_trips);
+            atomicAdd(pc + 6, ph_steps);
+            atomicAdd(pc + 7, ph_tbn);
+            atomicAdd(pc + 8, ph_idle);
         }
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(32 * KCfg<L>::WARPS, KCfg<L>::MINB)
+    k1_window_align(const __grid_constant__ AlignParams P) {
+    extern __shared__ uint32_t smem[];
+    const int wib = threadIdx.x >> 5;
+    k1_body<L, false>(P, smem + wib * warp_smem_words<L>(),
+                      static_cast<long long>(blockIdx.x) * KCfg<L>::WARPS + wib, nullptr, nullptr);
+}
+
+// K1 mixed (§3.8): band warps (K1b) and full-frame warps (limb count LF) in one
+// persistent block per SM, handing pairs to each other through P.q_full / P.q_band.
+// A full-frame warp of the mixed kernel: K1<LF> memory, its parked rows
+// [32 LF + 5][32][LF] and the STD windows' (EQ, parked) [68][32] uint2 — the same
+// words as the parked rows for LF = 2 (same per-lane mapping), after them for LF = 1.
+template <int LF> __host__ __device__ constexpr int mixed_eqp_offset() {
+    return LF == 2 ? 0 : (32 * LF + 5) * 32 * LF;
+}
+template <int LF> __host__ __device__ constexpr int mixed_full_words() {
+    return warp_smem_words<LF>() +
+           ((32 * LF + 5) * 32 * LF > mixed_eqp_offset<LF>() + band::eqp_words()
+                ? (32 * LF + 5) * 32 * LF : mixed_eqp_offset<LF>() + band::eqp_words());
+}
+template <int LF> __host__ __device__ constexpr int mixed_block_words() {
+    return band::WARPS * k1_warp_words<2, true>() + band::FWARPS * mixed_full_words<LF>();
+}
+template <int LF>
+__global__ void __launch_bounds__(32 * (band::WARPS + band::FWARPS), 1)
+    k1_mixed(const __grid_constant__ AlignParams P) {
+    extern __shared__ uint32_t smem[];
+    const int wib = threadIdx.x >> 5;
+    if (wib < band::WARPS) {
+        k1_body<2, true>(P, smem + wib * k1_warp_words<2, true>(),
+                         static_cast<long long>(blockIdx.x) * band::WARPS + wib, nullptr, nullptr);
+    } else {
+        const int fw = wib - band::WARPS;
+        uint32_t* const base = smem + band::WARPS * k1_warp_words<2, true>() + fw * mixed_full_words<LF>();
+        k1_body<LF, false>(P, base, static_cast<long long>(blockIdx.x) * band::FWARPS + fw,
+                           base + warp_smem_words<LF>(),
+                           base + warp_smem_words<LF>() + mixed_eqp_offset<LF>());
     }
 }
 
@@ -1012,6 +1531,24 @@ template <int L> int launch_L(const AlignParams& p, int grid, void* stream) {
     if (e != cudaSuccess) return static_cast<int>(e);
     k1_window_align<L><<<grid, 32 * KCfg<L>::WARPS, smem, static_cast<cudaStream_t>(stream)>>>(p);
     return static_cast<int>(cudaGetLastError());
+}
+
+template <int LF> int launch_mixed_L(const AlignParams& p, int grid, void* stream) {
+    const size_t smem = static_cast<size_t>(mixed_block_words<LF>()) * 4;
+    cudaError_t e = cudaFuncSetAttribute(k1_mixed<LF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    k1_mixed<LF><<<grid, 32 * (band::WARPS + band::FWARPS), smem,
+                   static_cast<cudaStream_t>(stream)>>>(p);
+    return static_cast<int>(cudaGetLastError());
+}
+
+__global__ void k1_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n) {
+    if (threadIdx.x < 32) {
+        q_band[threadIdx.x] = 0u;
+        q_full[threadIdx.x] = 0u;
+    }
+    if (threadIdx.x == 0) *remaining = static_cast<unsigned>(n);
 }
 
 // ------------------------------------------------------------------ K2 / K3
@@ -1108,6 +1645,40 @@ int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_blo
         case 4: return launch_L<4>(p, grid, stream);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
+}
+
+int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream) {
+    if (LF == 1) return launch_mixed_L<1>(p, grid, stream);
+    if (LF == 2) return launch_mixed_L<2>(p, grid, stream);
+    return static_cast<int>(cudaErrorInvalidValue);
+}
+
+int launch_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n, void* stream) {
+    k1_queue_init<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(q_band, q_full, remaining, n);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int mixed_band_warps() { return band::WARPS; }
+int mixed_full_warps() { return band::FWARPS; }
+
+int mixed_max_blocks_per_sm(int LF) {
+    int blocks = 0;
+    cudaError_t e;
+    if (LF == 1) {
+        const size_t smem = static_cast<size_t>(mixed_block_words<1>()) * 4;
+        cudaFuncSetAttribute(k1_mixed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<1>, 32 * (band::WARPS + band::FWARPS), smem);
+    } else {
+        const size_t smem = static_cast<size_t>(mixed_block_words<2>()) * 4;
+        cudaFuncSetAttribute(k1_mixed<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<2>, 32 * (band::WARPS + band::FWARPS), smem);
+    }
+    return e == cudaSuccess ? blocks : 0;
+}
+
+bool band_eligible(int W, int O, int single) {
+    return !single && W >= 4 && W <= band::WMAX && W % 4 == 0 && W - O >= 1 &&
+           W - O <= band::CMAX;
 }
 
 size_t bnd_scratch_bytes(int L, long long total_warps) {

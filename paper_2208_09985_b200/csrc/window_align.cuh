@@ -75,6 +75,12 @@ struct AlignParams {
     int64_t chunk_words;
     int32_t n_chunks;
     int32_t wcap;             // K6: widest window (columns) a warp's scratch holds
+    // K1 mixed: band warps (K1b) <-> full-frame warps
+    int32_t mixed;
+    uint32_t* q_band;         // pairs handed to band warps: [32 + n_pairs] (head, tail, slots)
+    uint32_t* q_full;         // pairs handed to full-frame warps
+    unsigned int* remaining;  // pairs not finished (warps exit at 0)
+    int32_t* resume_state;    // [n_pairs][4]: toff, poff, cur_op | cur_len << 8, open word
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
@@ -103,6 +109,17 @@ int launch_wide_align(const AlignParams& p, int grid, void* stream);
 int wide_warps_per_block();
 size_t wide_smem_bytes();
 int wide_max_blocks_per_sm();
+
+// K1 mixed: one persistent block per SM of band warps (K1b,
+// windows of W <= 64 columns in diagonal coordinates) and full-frame warps
+// (limb count LF); pairs move between them through device queues.
+int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream);
+int launch_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n,
+                      void* stream);
+int mixed_band_warps();
+int mixed_full_warps();
+int mixed_max_blocks_per_sm(int LF);
+bool band_eligible(int W, int O, int single);
 
 // K7 (csrc/exact_align.cu): optimal global alignment with the reference
 // oracle's tie-breaking (proj/src/oracle.cpp:39-89), one warp per pair.

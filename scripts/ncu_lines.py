@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 td = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_2208_09985_b200/_lib/libscrooge_b200.so")], cwd=td, capture_output=True)
 dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(td, "window_align.sm_100a.cubin")], capture_output=True, text=True).stdout
-sec = f"k1_window_alignILi{L}E"
+sec = os.environ.get("SG_SEC", f"k1_window_alignILi{L}E")
 addr_line, cur, inside = {}, None, False
 for ln in dis.split("\n"):
     if ".text." in ln and "//---" in ln:

@@ -21,8 +21,11 @@ print("cells_computed", r.total.cells_computed, "ALG_OPS/s (K1)", 4 * ((a.W + 31
 if os.environ.get("SG_PHASE_CYCLES") == "1":
     import ctypes as C
     from paper_2208_09985_b200 import _ffi
-    buf = (C.c_ulonglong * 8)()
+    buf = (C.c_ulonglong * 18)()
     _ffi.load().sg_debug_phase_cycles(buf)
-    tot = buf[0] + buf[1] + buf[2]
-    print(f"phase cycles (sum over warps): setup {buf[0]/tot:.1%}  DC {buf[1]/tot:.1%}  TB {buf[2]/tot:.1%}  iterations {buf[3]}  cycles/iter {tot/max(buf[3],1):.0f}")
-    print(f"lanes in DC per iteration {buf[4]/max(buf[3],1):.1f}/32  TB trips/iter {buf[5]/max(buf[3],1):.1f}  TB lane-steps/entry {buf[6]/max(buf[7],1):.1f}  TB entries/iter {buf[7]/max(buf[3],1):.1f}  TB lane-util {buf[6]/max(32*buf[5],1):.1%}")
+    for name, o in (("band/K1", 0), ("full", 9)):
+        b = buf[o:o + 9]
+        tot = b[0] + b[1] + b[2] + b[8]
+        if tot == 0: continue
+        print(f"{name}: cycles (sum over warps) {tot:.3e}: setup {b[0]/tot:.1%}  DC {b[1]/tot:.1%}  TB {b[2]/tot:.1%}  idle {b[8]/tot:.1%}  chunks {b[3]}  cycles/chunk {(b[0]+b[1]+b[2])/max(b[3],1):.0f}")
+        print(f"   lanes in DC per chunk {b[4]/max(b[3],1):.1f}/32  TB trips/chunk {b[5]/max(b[3],1):.1f}  TB lane-steps/entry {b[6]/max(b[7],1):.1f}  TB entries {b[7]}  TB lane-util {b[6]/max(32*b[5],1):.1%}")
