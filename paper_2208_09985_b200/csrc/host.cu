@@ -196,7 +196,7 @@ struct DevState {
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
-    DevBuf q_band, q_full, defer_count, resume_state;  // K1 mixed hand-over (§3.8)
+    DevBuf q_band, q_full, q_coop, q_std, defer_count, resume_state;  // K1 mixed hand-over (§3.8)
     long long grid = 0, lanes = 0;
 
     void init(int dev) {
@@ -215,7 +215,7 @@ struct DevState {
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
-                          &q_band, &q_full, &defer_count, &resume_state})
+                          &q_band, &q_full, &q_coop, &q_std, &defer_count, &resume_state})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
@@ -682,6 +682,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         st.lanes = grid_band * sgk::mixed_band_warps() * 32;
         st.q_band.ensure(4 * (n1 + 32));
         st.q_full.ensure(4 * (n1 + 32));
+        st.q_coop.ensure(4 * (n1 + 32));
+        st.q_std.ensure(4 * (n1 + 32));
         st.defer_count.ensure(64);
         st.resume_state.ensure(16 * n1);
     }
@@ -737,7 +739,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
             SG_CUDA_CHECK(cudaMemsetAsync(wbuf, 0, 8 * 3 * 8192, st.stream));
             p.warp_times = wbuf;
             g_warp_times = wbuf;
-            g_warp_count = static_cast<int>(grid * wpb);
+            g_warp_count = static_cast<int>(rc.band ? grid_band * 8 : grid * wpb);
         }
     }
     if (const char* e = getenv("SG_PHASE_CYCLES")) {
@@ -759,12 +761,16 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         p.mixed = 1;
         p.q_band = st.q_band.as<uint32_t>();
         p.q_full = st.q_full.as<uint32_t>();
+        p.q_coop = st.q_coop.as<uint32_t>();
+        p.q_std = st.q_std.as<uint32_t>();
         p.remaining = st.defer_count.as<unsigned int>();
         p.resume_state = st.resume_state.as<int32_t>();
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_band.p, 0, st.q_band.cap, st.stream));
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_full.p, 0, st.q_full.cap, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.q_coop.p, 0, st.q_coop.cap, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.q_std.p, 0, st.q_std.cap, st.stream));
         SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_queue_init(
-            p.q_band, p.q_full, p.remaining, static_cast<int>(n), st.stream)));
+            p.q_band, p.q_full, p.q_coop, p.q_std, p.remaining, static_cast<int>(n), st.stream)));
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
         launches += 2;
@@ -1319,7 +1325,7 @@ int sg_debug_warp_times(unsigned long long* out, int cap) {
 
 int sg_debug_phase_cycles(unsigned long long* out8) {
     if (!g_phase_buf) return -1;
-    cudaMemcpy(out8, g_phase_buf, 18 * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out8, g_phase_buf, 25 * 8, cudaMemcpyDeviceToHost);
     return 0;
 }
 

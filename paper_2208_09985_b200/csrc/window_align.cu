@@ -781,6 +781,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     int last_d = 0;        // D(0, 0) of the last window
     bool defer_now = false;
     bool std_win = false;  // full-frame warp, mixed: the window runs in the STD frame (m_w <= 31)
+    int hand_to = 0;       // mixed: the role the pair goes to (0 band, 1 full frame, 2 cooperative)
     // Sequence staging: sq_t / sq_p hold PFW packed words from word st_tw / st_pw;
     // the segment's text / pattern start at base t_sh / p_sh inside them. The
     // words of the region the next window can start in are prefetched into
@@ -880,20 +881,20 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             load_bits<L + 1>(P.nmask, pbase + poff, pn);
             load_bits<L + 1>(P.nmask, tbase + toff, tn);
         }
-        if (!BAND && std_win) {
+        if (std_win) {
             // (§3.8) STD frame: EQ_i = plane t_i of the pattern, bits j < m_w <= 31;
-            // the planes go to this lane's pattern-mask slots, the parked row
-            // starts as row -1 (zeros)
+            // the planes go to this lane's event columns 0..3 (dead until the first
+            // chunk overwrites them), the parked row starts as row -1 (zeros)
             const uint32_t lo = compress_stride<2>(pw[0] & 0x55555555u) |
                                 (compress_stride<2>(pw[1] & 0x55555555u) << 16);
             const uint32_t hi = compress_stride<2>((pw[0] >> 1) & 0x55555555u) |
                                 (compress_stride<2>((pw[1] >> 1) & 0x55555555u) << 16);
             const uint32_t valid = ((1u << m_w) - 1u) & ~pn[0];
-            uint32_t* const pl = pmv + lane * L;  // [5][32][L] words, limb 0 used
-            pl[0 * 32 * L] = ~lo & ~hi & valid;
-            pl[1 * 32 * L] = lo & ~hi & valid;
-            pl[2 * 32 * L] = ~lo & hi & valid;
-            pl[3 * 32 * L] = lo & hi & valid;  // (code 4's all-ones full-frame mask stays)
+            uint32_t* const pl = xy + lane * 2;  // column c at pl[c * 64]
+            pl[0 * 64] = ~lo & ~hi & valid;
+            pl[1 * 64] = lo & ~hi & valid;
+            pl[2 * 64] = ~lo & hi & valid;
+            pl[3 * 64] = lo & hi & valid;
             for (int k = 0; 16 * k < n_w; ++k) {
                 const int bt = t_sh + 16 * k;
                 const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
@@ -903,7 +904,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int code = static_cast<int>((tword >> (2 * u)) & 3u);
-                    uint32_t e = pl[code * 32 * L];
+                    uint32_t e = pl[code * 64];
                     if (hasn && ((tnw >> u) & 1u)) e = 0u;  // non-ACGT text matches nothing
                     bmem.eqp[(16 * k + u + 4) * 32] = make_uint2(e, 0u);
                 }
@@ -1034,14 +1035,35 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         {
             const int dl = m_w - n_w;
             const bool band_ok = !fin && n_w == W && dl <= band::kLastRow && dl >= -band::kLastRow;
+            // full-width non-final windows the single-word frames cannot take go
+            // to a cooperative warp (§3.9)
+            const bool wide_ok = !fin && n_w == W && m_w >= 32;
+            const bool std_ok = !fin && n_w == W && m_w <= 31;  // the STD frame takes it
+            std_win = false;
             if (BAND) {
-                if (!band_ok) return 2;
-                e_lo = (dl >> 1) - 16;
-                K0 = dl - e_lo;
+                if (!band_ok) {
+                    // STD windows stay in this lane once no fresh pairs are left (the
+                    // end of the batch: full-frame warps alone would drain them slowly)
+                    if (std_ok && *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
+                                      static_cast<unsigned>(P.n_pairs)) {
+                        std_win = true;
+                    } else {
+                        hand_to = wide_ok ? 2 : std_ok ? 3 : 1;
+                        return 2;
+                    }
+                } else {
+                    e_lo = (dl >> 1) - 16;
+                    K0 = dl - e_lo;
+                }
             } else if (P.mixed && band_ok && pass_win > 0 && last_d <= band::kBackRow) {
+                hand_to = 0;
                 return 2;  // back on track: the band frame takes the pair again
+            } else if (P.mixed && wide_ok) {
+                hand_to = 2;
+                return 2;
+            } else {
+                std_win = bnd_smem != nullptr && std_ok;
             }
-            std_win = !BAND && bnd_smem != nullptr && !fin && n_w == W && m_w <= 31;
         }
         limit = fin ? -1 : step_limit;
         first_seg = true;
@@ -1071,7 +1093,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         rs[1] = poff;
         rs[2] = (cur_op & 0xFF) | (cur_len << 8);
         rs[3] = static_cast<int32_t>(acc);
-        q_push(BAND ? P.q_full : P.q_band, P.n_pairs, pair);
+        q_push(hand_to == 0 ? P.q_band : hand_to == 1 ? P.q_full : hand_to == 2 ? P.q_coop : P.q_std,
+               P.n_pairs, pair);
     };
 
     auto finish_pair = [&]() {
@@ -1100,6 +1123,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         bool restore = false;
         if (P.mixed) {  // a pair handed over by the other frame first
             pair = q_pop(BAND ? P.q_band : P.q_full, P.n_pairs);
+            if (pair < 0 && (!BAND || *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
+                                          static_cast<unsigned>(P.n_pairs)))
+                pair = q_pop(P.q_std, P.n_pairs);  // band warps: once no fresh pairs are left
             restore = pair >= 0;
         }
         if (BAND || !P.mixed) {  // fresh pairs (warp-aggregated claim)
@@ -1198,7 +1224,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     unsigned long long last_busy = 0;
     bool need_pair = true, need_window = false, need_load = false;
     unsigned long long ph_setup = 0, ph_dc = 0, ph_tb = 0, ph_it = 0, ph_act = 0, ph_trips = 0,
-                       ph_steps = 0, ph_tbn = 0, ph_idle = 0;
+                       ph_steps = 0, ph_tbn = 0, ph_idle = 0, ph_std = 0, ph_ffc = 0, ph_ffl = 0;
     for (;;) {
         const long long ck0 = clock64();
         // ---------------------------------------------- per-lane setup
@@ -1233,15 +1259,15 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         const bool in_dc = pair >= 0;
         if (!__any_sync(kFull, in_dc)) {
             if (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
-            if (P.warp_times && lane == 0 && last_busy == 0) {  // diagnostics: first idle moment
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_busy));
-            }
+
             // pairs are still in flight: one may be handed to this warp
             __nanosleep(BAND ? 2000 : 8000);
             ph_idle += clock64() - ck0;
             continue;
         }
         __syncwarp();
+        if (P.warp_times && lane == 0)  // diagnostics: the last iteration with work
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(last_busy));
         const long long ck1 = clock64();
 
         // ------------------------------------------------ DC chunks + d_opt detection
@@ -1252,15 +1278,31 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             const bool act = in_dc && !solved;
             if (sub > 0 && !__any_sync(kFull, act)) break;
             if constexpr (BAND) {
-                const int fr = band_chunk<false>(act, d0, W, cmax, K0, -e_lo, bmem, two, hmul);
+                const bool act_b = act && !std_win, act_s = act && std_win;
+                int fr = -1;
+                if (__any_sync(kFull, act_b)) {
+                    const int f = band_chunk<false>(act_b, d0, W, cmax, K0, -e_lo, bmem, two, hmul);
+                    if (act_b) fr = f;
+                }
+                if (__any_sync(kFull, act_s)) {
+                    const int f = band_chunk<true>(act_s, d0, W, cmax, m_w, 0, bmem, two, hmul);
+                    if (act_s) fr = f;
+                }
                 ++ph_it;
                 ph_act += __popc(__ballot_sync(kFull, act));
-                if (act) {
+                if (act && std_win) {  // the STD frame is exact for every row
+                    if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
+                    solved = found_d >= 0 || d0 + R > K;
+                    if (!solved) d0 += R;
+                } else if (act) {
                     if (found_d < 0 && fr >= 0) found_d = d0 + fr;
                     // D(0, 0) is exact up to band_last; beyond it the window goes
-                    // to the full frame (resume pass)
+                    // to a cooperative warp
                     solved = found_d >= 0 || d0 + R > band_last;
-                    if (solved && (found_d < 0 || found_d > band_last)) defer_now = true;
+                    if (solved && (found_d < 0 || found_d > band_last)) {
+                        defer_now = true;
+                        hand_to = 2;
+                    }
                     if (!solved) d0 += R;
                 }
                 continue;
@@ -1273,6 +1315,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     if (act_std) fr = f;
                     ++ph_it;
                     ph_act += __popc(__ballot_sync(kFull, act_std));
+                    ph_std += __popc(__ballot_sync(kFull, act_std));
                 }
             }
             const bool act_full = act && !std_win;
@@ -1281,6 +1324,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 const int f = dc_chunk<L, R, C>(act_full ? n_w : 0, act_full, m_w, act_full ? d0 : 0,
                                                 n_max, two, one, lmem);
                 if (act_full) fr = f;
+                ph_ffc += 1;
+                ph_ffl += __popc(__ballot_sync(kFull, act_full));
             }
             ++ph_it;
             ph_act += __popc(__ballot_sync(kFull, act));
@@ -1377,7 +1422,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 // the edit at the mismatch (i, j)
                 const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
                 uint32_t bit;
-                if constexpr (BAND) {  // diagonal band: cell (i, j) at bit j - i - e_lo
+                if (BAND && std_win) {
+                    bit = 1u << j;
+                } else if constexpr (BAND) {  // diagonal band: cell (i, j) at bit j - i - e_lo
                     const int kb = j - i - e_lo;
                     if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
                         status = kStInternal | kDetSegment;
@@ -1473,7 +1520,372 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             atomicAdd(pc + 6, ph_steps);
             atomicAdd(pc + 7, ph_tbn);
             atomicAdd(pc + 8, ph_idle);
+            if (!BAND) {
+                atomicAdd(P.phase_cycles + 18, ph_std);
+                atomicAdd(P.phase_cycles + 19, ph_ffc);
+                atomicAdd(P.phase_cycles + 20, ph_ffl);
+            }
         }
+    }
+}
+
+// ------------------------------------------------------ K1c: cooperative windows
+//
+// DESIGN.md §3.9. One warp computes one window of W <= 64 columns: the standard
+// frame with 64-bit rows (bit j = cell (i, j), complemented: 1 <=> D(i, j) <= d),
+// lane r computes row 32p + r of pass p, one column per step, one column behind
+// lane r - 1 (its north neighbour arrives by shuffle; lane 0 reads the previous
+// pass's last row). Cell update (dp.cpp:187-211 in these coordinates):
+//   C[i][d] = (sh(C[i+1][d]) & EQ_i) | C[i+1][d-1] | sh(C[i+1][d-1]) | sh(C[i][d-1])
+// with sh(x) = x >> 1 and, when m_w = 64, the end-of-pattern cell D(i', 64) =
+// n_w - i' shifted in at bit 63 (dp.hpp:145-154). Traceback events X / Y of
+// every row are OR-ed into shared memory (atom.shared.or.b64), so the traceback
+// is K1's. Used for the full-width windows the single-word frames cannot take
+// (D(0, 0) > 30, or 32 <= m_w with |m_w - n_w| > 30): 30..60 rows in one or
+// two passes instead of 8..16 sequential 4-row chunks on one lane.
+namespace coop {
+constexpr int kWords = 66 * 2 + 66 * 2 + 65 * 4 + 20;  // eq, prow, xy (+ dummies), staging
+}
+
+__device__ __forceinline__ uint64_t shr1_in(uint64_t x, uint32_t b) {
+    return (x >> 1) | (static_cast<uint64_t>(b) << 63);
+}
+
+// init column (i = n_w) of row d: bits j in [m - d, m] (bit 64 = the boundary, implicit)
+__device__ __forceinline__ uint64_t coop_init(int d, int m) {
+    if (d < 0) return 0ull;
+    const int lo = max(m - d, 0);
+    const uint64_t top = m >= 63 ? ~0ull : ((2ull << m) - 1ull);
+    return lo >= 64 ? 0ull : (top & (~0ull << lo));
+}
+
+__device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
+    const int lane = threadIdx.x & 31;
+    uint2* const eqs = reinterpret_cast<uint2*>(sm);             // [64 + dummy] EQ_i
+    uint2* const prow = eqs + 66;                                // [64 + 2 dummies] last row of the pass
+    uint4* const xys = reinterpret_cast<uint4*>(prow + 66);      // [64 + dummy] X lo, X hi, Y lo, Y hi
+    uint32_t* const st = reinterpret_cast<uint32_t*>(xys + 65);  // text [6], pattern [6], tn [3], pn [3]
+    const int W = P.W, step_limit = W - P.O, K = W;
+    const long long dwarp = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (P.warp_times && lane == 0) {  // diagnostics: start, last window's end
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.warp_times[dwarp * 3] = t;
+        P.warp_times[dwarp * 3 + 1] = t;
+    }
+    for (;;) {
+        int pair = -1;
+        if (lane == 0) pair = q_pop(P.q_coop, P.n_pairs);
+        pair = __shfl_sync(kFull, pair, 0);
+        if (pair < 0) {
+            if (*reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
+            __nanosleep(4000);
+            continue;
+        }
+        // ---- restore the pair (every lane holds the same state; lane 0 writes)
+        const int n_tot = P.text_len[pair], m_tot = P.pat_len[pair];
+        const int64_t tbase = P.text_off[pair], pbase = P.pat_off[pair];
+        const bool hasn = P.has_n ? P.has_n[pair] != 0 : false;
+        const int4 rs = __ldcg(reinterpret_cast<const int4*>(P.resume_state + 4ll * pair));
+        int toff = rs.x, poff = rs.y;
+        int cur_op = (rs.z & 0xFF) == 0xFF ? -1 : (rs.z & 0xFF), cur_len = rs.z >> 8;
+        uint32_t acc = static_cast<uint32_t>(rs.w);
+        int dist = __ldcg(P.distance + pair), nwin = __ldcg(P.windows + pair);
+        int out_bytes = __ldcg(P.out_bytes + pair), acc_n = out_bytes & 3, status = 0;
+        uint32_t* outw = P.scratch + (P.bound_off[pair] >> 2) + (out_bytes >> 2);
+        unsigned long long cn[7] = {0, 0, 0, 0, 0, 0, 0};
+        if (P.counters) {
+            const unsigned long long* c =
+                reinterpret_cast<const unsigned long long*>(P.counters + 7ll * pair);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) cn[k] = __ldcg(c + k);
+        }
+        const int window_cap = 4 * ((n_tot + m_tot) / step_limit + 2);  // aligner.cpp:40
+        auto put_byte = [&](uint32_t b) {
+            acc |= b << (8 * acc_n);
+            ++out_bytes;
+            if (++acc_n == 4) {
+                if (lane == 0) *outw = acc;
+                ++outw;
+                acc = 0;
+                acc_n = 0;
+            }
+        };
+        auto emit = [&](int op, int len) {  // cigar_append (cigar.cpp:9-16) as run bytes
+            if (op == cur_op && cur_len + len <= 64) {
+                cur_len += len;
+                return;
+            }
+            if (op == cur_op) {
+                len -= 64 - cur_len;
+                cur_len = 64;
+            }
+            if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
+            while (len > 64) {
+                put_byte((static_cast<uint32_t>(op) << 6) | 63u);
+                len -= 64;
+            }
+            cur_op = op;
+            cur_len = len;
+        };
+        int hand = -1;  // -1 finished, 0 band, 1 full frame
+        int last_d = 0, pass_win = 0;
+        for (;;) {
+            // ---- next window (aligner.cpp:44-64)
+            const int n_rem = n_tot - toff, m_rem = m_tot - poff;
+            if (n_rem == 0 || m_rem == 0) {
+                if (n_rem + m_rem > 0) {  // aligner.cpp:48-57
+                    emit(n_rem == 0 ? 2 : 3, n_rem + m_rem);
+                    dist += n_rem + m_rem;
+                }
+                break;
+            }
+            const bool fin = n_rem <= W && m_rem <= W;
+            const int n_w = min(W, n_rem), m_w = min(W, m_rem), dl = m_w - n_w;
+            const bool band_ok = !fin && n_w == W && dl <= band::kLastRow && dl >= -band::kLastRow;
+            if (pass_win > 0 && band_ok && last_d <= band::kBackRow) { hand = 0; break; }
+            if (fin || n_w != W || m_w < 32) { hand = !fin && n_w == W ? 3 : 1; break; }
+            const long long cw0 = clock64();
+            // ---- staging: the window's packed text / pattern (bases 16k.. in word k) and N bits
+            {
+                const int64_t ta = tbase + toff, pa = pbase + poff;
+                const uint32_t rt = lane < 7 ? __ldcg(P.seq + (ta >> 4) + lane) : 0u;
+                const uint32_t rp = lane < 7 ? __ldcg(P.seq + (pa >> 4) + lane) : 0u;
+                const uint32_t rt1 = __shfl_down_sync(kFull, rt, 1), rp1 = __shfl_down_sync(kFull, rp, 1);
+                if (lane < 6) {
+                    st[lane] = __funnelshift_r(rt, rt1, 2 * static_cast<int>(ta & 15));
+                    st[6 + lane] = __funnelshift_r(rp, rp1, 2 * static_cast<int>(pa & 15));
+                }
+                uint32_t tn = 0, pn = 0;
+                if (hasn) {
+                    const int64_t a = lane < 3 ? ta : pa;
+                    const int k = lane < 3 ? lane : lane - 3;
+                    const uint32_t r0 = lane < 6 ? __ldcg(P.nmask + (a >> 5) + k) : 0u;
+                    const uint32_t r1 = lane < 6 ? __ldcg(P.nmask + (a >> 5) + k + 1) : 0u;
+                    const uint32_t w = __funnelshift_r(r0, r1, static_cast<int>(a & 31));
+                    if (lane < 3) tn = w; else pn = w;
+                }
+                if (lane < 3) st[12 + lane] = tn;
+                else if (lane < 6) st[15 + lane - 3] = pn;
+                // events start empty; column lane and lane + 32
+                xys[lane] = make_uint4(0u, 0u, 0u, 0u);
+                xys[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            __syncwarp();
+            // pattern code planes (64 bits, j < m_w, no N) and EQ_i of columns lane, lane + 32
+            {
+                uint64_t lo = 0, hi = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t w = st[6 + k];
+                    lo |= static_cast<uint64_t>(compress_stride<2>(w & 0x55555555u)) << (16 * k);
+                    hi |= static_cast<uint64_t>(compress_stride<2>((w >> 1) & 0x55555555u)) << (16 * k);
+                }
+                uint64_t valid = m_w >= 64 ? ~0ull : ((1ull << m_w) - 1ull);
+                if (hasn) valid &= ~(static_cast<uint64_t>(st[15]) | (static_cast<uint64_t>(st[16]) << 32));
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int i = lane + 32 * h;
+                    const int code = static_cast<int>((st[i >> 4] >> (2 * (i & 15))) & 3u);
+                    const uint64_t l = code & 1 ? lo : ~lo, g = code & 2 ? hi : ~hi;
+                    uint64_t e = l & g & valid;
+                    if (hasn && ((st[12 + (i >> 5)] >> (i & 31)) & 1u)) e = 0ull;
+                    eqs[i] = make_uint2(static_cast<uint32_t>(e), static_cast<uint32_t>(e >> 32));
+                }
+            }
+            __syncwarp();
+            // ---- DC: passes of 32 rows
+            int found = -1;
+            for (int p = 0; 32 * p <= K && found < 0; ++p) {
+                const int d = 32 * p + lane;
+                uint64_t v = coop_init(d, m_w), dg = coop_init(d - 1, m_w);
+                bool f0 = false;
+                // branch-free steps: inactive lanes (not started / finished) keep
+                // their state; their event and row stores go to the dummy slots
+                const uint64_t pmask = p > 0 ? ~0ull : 0ull;
+                for (int s = 0; s < n_w + 31; ++s) {
+                    const uint32_t ul = __shfl_up_sync(kFull, static_cast<uint32_t>(v), 1);
+                    const uint32_t uh = __shfl_up_sync(kFull, static_cast<uint32_t>(v >> 32), 1);
+                    const int col = n_w - 1 - s + lane;
+                    const bool act = lane <= s && col >= 0;
+                    const int cs = act ? col : 64;  // column slot (64 = dummy)
+                    const uint2 pr = prow[cs];
+                    const uint2 e2 = eqs[cs];
+                    uint64_t north = (static_cast<uint64_t>(uh) << 32) | ul;
+                    if (lane == 0) north = ((static_cast<uint64_t>(pr.y) << 32) | pr.x) & pmask;
+                    const uint64_t eq = (static_cast<uint64_t>(e2.y) << 32) | e2.x;
+                    uint32_t be = 0, bs = 0, bn = 0;
+                    if (m_w == 64) {  // D(i', 64) = n_w - i' <= d' shifted in at bit 63
+                        const int c = n_w - col;
+                        be = c - 1 <= d;
+                        bs = c - 1 <= d - 1;
+                        bn = c <= d - 1;
+                    }
+                    const uint64_t mt = shr1_in(v, be);
+                    const uint64_t nc = (mt & eq) | dg | shr1_in(dg, bs) | shr1_in(north, bn);
+                    {   // events: at one step the lanes are on different columns and lane
+                        // r + 1 reaches a column one step after lane r, so the
+                        // read-modify-write is race-free
+                        const uint64_t x = mt & ~nc, y = v & ~nc;
+                        const int es = act && col < step_limit ? col : 64;
+                        uint4 o = xys[es];
+                        o.x |= static_cast<uint32_t>(x);
+                        o.y |= static_cast<uint32_t>(x >> 32);
+                        o.z |= static_cast<uint32_t>(y);
+                        o.w |= static_cast<uint32_t>(y >> 32);
+                        xys[es] = o;
+                    }
+                    prow[lane == 31 ? cs : 65] = make_uint2(static_cast<uint32_t>(nc),
+                                                            static_cast<uint32_t>(nc >> 32));
+                    f0 |= act && col == 0 && (nc & 1ull);
+                    dg = act ? north : dg;
+                    v = act ? nc : v;
+                }
+                const unsigned fb = __ballot_sync(kFull, f0 && d <= K);
+                if (fb) found = 32 * p + __ffs(fb) - 1;
+                __syncwarp();
+            }
+            const long long cw1 = clock64();
+            if (found < 0) {  // D(0, 0) > K (aligner.cpp:69-70)
+                status = kStInternal | kDetNoStep;
+                break;
+            }
+            // reference counters of the window (dp.cpp:23-37,58-75,225-228)
+            {
+                const int rows_ref = P.et ? found + 1 : K + 1;
+                const int pol = P.policy;
+                int keep_cols = n_w + 1, keep_bits = m_w;
+                if (pol == 2) {
+                    keep_cols = min(n_w, step_limit) + 1;
+                    keep_bits = min(m_w, step_limit + 1);
+                }
+                const unsigned long long slots = pol == 0 ? 3ull : 1ull;
+                cn[0] += static_cast<unsigned long long>(rows_ref) * keep_cols * keep_bits * slots;
+                cn[1] += static_cast<unsigned long long>(rows_ref) * keep_cols * slots;
+                cn[3] += rows_ref;
+                cn[4] += static_cast<unsigned long long>(rows_ref) * n_w;
+                cn[6] += 3ull * (n_w + 1) * static_cast<unsigned long long>(K + 1) * m_w;
+            }
+            // ---- TB (traceback.cpp:56-113), uniform over the lanes
+            int i = 0, j = 0, d = found, steps = 0;
+            unsigned reads = 0;
+            for (;;) {
+                int rem = step_limit - steps;
+                if (rem == 0 || i == n_w || j == m_w) break;
+                int run;
+                {   // matching bases from (i, j) on
+                    const uint32_t tw = __funnelshift_r(st[i >> 4], st[(i >> 4) + 1], 2 * (i & 15));
+                    const uint32_t pw = __funnelshift_r(st[6 + (j >> 4)], st[6 + (j >> 4) + 1], 2 * (j & 15));
+                    uint32_t x = tw ^ pw;
+                    x = (x | (x >> 1)) & 0x55555555u;
+                    if (hasn) {
+                        const uint32_t tn = __funnelshift_r(st[12 + (i >> 5)], st[13 + (i >> 5)], i & 31);
+                        const uint32_t pn = __funnelshift_r(st[15 + (j >> 5)], st[16 + (j >> 5)], j & 31);
+                        uint32_t q = (tn | pn) & 0xFFFFu;
+                        q = (q | (q << 8)) & 0x00FF00FFu;
+                        q = (q | (q << 4)) & 0x0F0F0F0Fu;
+                        q = (q | (q << 2)) & 0x33333333u;
+                        q = (q | (q << 1)) & 0x55555555u;
+                        x |= q;
+                    }
+                    run = __clz(__brev(x)) >> 1;
+                }
+                const int k = min(min(run, rem), min(n_w - i, m_w - j));
+                if (k > 0) {
+                    reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
+                    i += k;
+                    j += k;
+                    steps += k;
+                    rem -= k;
+                    emit(0, k);
+                }
+                if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w) continue;
+                const uint4 ev = xys[i];
+                const uint32_t xw = j < 32 ? ev.x : ev.y, yw = j < 32 ? ev.z : ev.w;
+                const int op = (xw >> (j & 31)) & 1u ? 1 : ((yw >> (j & 31)) & 1u ? 3 : 2);
+                if (d == 0) status = kStInternal | kDetNoStep;
+                reads += d == 0 ? 1u : 3u;
+                i += op != 2;
+                j += op != 3;
+                --d;
+                ++dist;
+                ++steps;
+                emit(op, 1);
+            }
+            {   // one side consumed: a single run of indels (traceback.cpp:76-86)
+                const int rem = step_limit - steps;
+                if (rem > 0 && !(i == n_w && j == m_w) && (i == n_w || j == m_w)) {
+                    const int op = i == n_w ? 2 : 3;
+                    const int left = i == n_w ? m_w - j : n_w - i;
+                    if (d != left) status = kStInternal | (i == n_w ? kDetBudgetI : kDetBudgetD);
+                    const int k = min(rem, left);
+                    i += op != 2 ? k : 0;
+                    j += op != 3 ? k : 0;
+                    dist += k;
+                    emit(op, k);
+                }
+            }
+            cn[2] += reads;
+            toff += i;
+            poff += j;
+            ++nwin;
+            ++pass_win;
+            last_d = found;
+            if (P.warp_times && lane == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                P.warp_times[dwarp * 3 + 1] = t;
+            }
+            if (P.phase_cycles && lane == 0) {
+                atomicAdd(P.phase_cycles + 21, 1ull);
+                atomicAdd(P.phase_cycles + 22, static_cast<unsigned long long>(cw1 - cw0));
+                atomicAdd(P.phase_cycles + 23, static_cast<unsigned long long>(clock64() - cw1));
+                atomicAdd(P.phase_cycles + 24, static_cast<unsigned long long>(found));
+            }
+            if (nwin > window_cap) status = kStInternal | kDetWatchdog;
+            if (status) break;
+            __syncwarp();
+        }
+        // ---- finish the pair or hand it on
+        if (lane == 0) {
+            if (hand < 0) {
+                if (cur_op >= 0) {
+                    acc |= ((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1)) << (8 * acc_n);
+                    ++out_bytes;
+                    *outw = acc;
+                } else if (acc_n) {
+                    *outw = acc;
+                }
+                P.distance[pair] = dist;
+                P.windows[pair] = nwin;
+                P.status[pair] = status;
+                P.out_bytes[pair] = out_bytes;
+                if (P.counters) {
+                    uint64_t* c = P.counters + 7ll * pair;
+#pragma unroll
+                    for (int k = 0; k < 7; ++k) c[k] = cn[k];
+                    c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
+                }
+                atomicSub(P.remaining, 1u);
+            } else {
+                P.distance[pair] = dist;
+                P.windows[pair] = nwin;
+                P.status[pair] = 0;
+                P.out_bytes[pair] = out_bytes;
+                if (P.counters) {
+                    uint64_t* c = P.counters + 7ll * pair;
+#pragma unroll
+                    for (int k = 0; k < 7; ++k) c[k] = cn[k];
+                }
+                int32_t* r = P.resume_state + 4ll * pair;
+                r[0] = toff;
+                r[1] = poff;
+                r[2] = (cur_op & 0xFF) | (cur_len << 8);
+                r[3] = static_cast<int32_t>(acc);
+                q_push(hand == 0 ? P.q_band : hand == 1 ? P.q_full : P.q_std, P.n_pairs, pair);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -1500,14 +1912,19 @@ template <int LF> __host__ __device__ constexpr int mixed_full_words() {
                 ? (32 * LF + 5) * 32 * LF : mixed_eqp_offset<LF>() + band::eqp_words());
 }
 template <int LF> __host__ __device__ constexpr int mixed_block_words() {
-    return band::WARPS * k1_warp_words<2, true>() + band::FWARPS * mixed_full_words<LF>();
+    return band::WARPS * k1_warp_words<2, true>() + band::FWARPS * mixed_full_words<LF>() +
+           coop::kWords;
 }
+constexpr int kMixedWarps = band::WARPS + band::FWARPS + 1;  // + one cooperative warp
 template <int LF>
-__global__ void __launch_bounds__(32 * (band::WARPS + band::FWARPS), 1)
+__global__ void __launch_bounds__(32 * kMixedWarps, 1)
     k1_mixed(const __grid_constant__ AlignParams P) {
     extern __shared__ uint32_t smem[];
     const int wib = threadIdx.x >> 5;
-    if (wib < band::WARPS) {
+    if (wib == kMixedWarps - 1) {
+        coop_body(P, smem + band::WARPS * k1_warp_words<2, true>() +
+                         band::FWARPS * mixed_full_words<LF>());
+    } else if (wib < band::WARPS) {
         k1_body<2, true>(P, smem + wib * k1_warp_words<2, true>(),
                          static_cast<long long>(blockIdx.x) * band::WARPS + wib, nullptr, nullptr);
     } else {
@@ -1538,15 +1955,18 @@ template <int LF> int launch_mixed_L(const AlignParams& p, int grid, void* strea
     cudaError_t e = cudaFuncSetAttribute(k1_mixed<LF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
-    k1_mixed<LF><<<grid, 32 * (band::WARPS + band::FWARPS), smem,
+    k1_mixed<LF><<<grid, 32 * kMixedWarps, smem,
                    static_cast<cudaStream_t>(stream)>>>(p);
     return static_cast<int>(cudaGetLastError());
 }
 
-__global__ void k1_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n) {
+__global__ void k1_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop,
+                              uint32_t* q_std, unsigned* remaining, int n) {
     if (threadIdx.x < 32) {
         q_band[threadIdx.x] = 0u;
         q_full[threadIdx.x] = 0u;
+        q_coop[threadIdx.x] = 0u;
+        q_std[threadIdx.x] = 0u;
     }
     if (threadIdx.x == 0) *remaining = static_cast<unsigned>(n);
 }
@@ -1653,8 +2073,10 @@ int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream) {
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
-int launch_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n, void* stream) {
-    k1_queue_init<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(q_band, q_full, remaining, n);
+int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint32_t* q_std,
+                      unsigned* remaining, int n, void* stream) {
+    k1_queue_init<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(q_band, q_full, q_coop, q_std,
+                                                                  remaining, n);
     return static_cast<int>(cudaGetLastError());
 }
 
@@ -1667,11 +2089,11 @@ int mixed_max_blocks_per_sm(int LF) {
     if (LF == 1) {
         const size_t smem = static_cast<size_t>(mixed_block_words<1>()) * 4;
         cudaFuncSetAttribute(k1_mixed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<1>, 32 * (band::WARPS + band::FWARPS), smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<1>, 32 * kMixedWarps, smem);
     } else {
         const size_t smem = static_cast<size_t>(mixed_block_words<2>()) * 4;
         cudaFuncSetAttribute(k1_mixed<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<2>, 32 * (band::WARPS + band::FWARPS), smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k1_mixed<2>, 32 * kMixedWarps, smem);
     }
     return e == cudaSuccess ? blocks : 0;
 }

@@ -79,6 +79,8 @@ struct AlignParams {
     int32_t mixed;
     uint32_t* q_band;         // pairs handed to band warps: [32 + n_pairs] (head, tail, slots)
     uint32_t* q_full;         // pairs handed to full-frame warps
+    uint32_t* q_coop;         // pairs handed to the cooperative warps (one window per warp)
+    uint32_t* q_std;          // pairs whose next window the STD frame takes (m_w <= 31)
     unsigned int* remaining;  // pairs not finished (warps exit at 0)
     int32_t* resume_state;    // [n_pairs][4]: toff, poff, cur_op | cur_len << 8, open word
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
@@ -114,8 +116,8 @@ int wide_max_blocks_per_sm();
 // windows of W <= 64 columns in diagonal coordinates) and full-frame warps
 // (limb count LF); pairs move between them through device queues.
 int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream);
-int launch_queue_init(uint32_t* q_band, uint32_t* q_full, unsigned* remaining, int n,
-                      void* stream);
+int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint32_t* q_std,
+                      unsigned* remaining, int n, void* stream);
 int mixed_band_warps();
 int mixed_full_warps();
 int mixed_max_blocks_per_sm(int LF);

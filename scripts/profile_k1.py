@@ -10,8 +10,9 @@ ap.add_argument("--pairs", type=int, default=100000)
 ap.add_argument("--W", type=int, default=64)
 ap.add_argument("--O", type=int, default=24)
 ap.add_argument("--runs", type=int, default=2)
+ap.add_argument("--seed", type=int, default=0)
 a = ap.parse_args()
-batch = sg.synth_packed(a.cfg, 0, a.pairs)
+batch = sg.synth_packed(a.cfg, a.seed, a.pairs)
 s = sg.Session(sg.AlignerConfig(W=a.W, O=a.O), batch)
 for _ in range(a.runs):
     ms, k1 = s.run()
@@ -21,7 +22,7 @@ print("cells_computed", r.total.cells_computed, "ALG_OPS/s (K1)", 4 * ((a.W + 31
 if os.environ.get("SG_PHASE_CYCLES") == "1":
     import ctypes as C
     from paper_2208_09985_b200 import _ffi
-    buf = (C.c_ulonglong * 18)()
+    buf = (C.c_ulonglong * 25)()
     _ffi.load().sg_debug_phase_cycles(buf)
     for name, o in (("band/K1", 0), ("full", 9)):
         b = buf[o:o + 9]
@@ -29,3 +30,5 @@ if os.environ.get("SG_PHASE_CYCLES") == "1":
         if tot == 0: continue
         print(f"{name}: cycles (sum over warps) {tot:.3e}: setup {b[0]/tot:.1%}  DC {b[1]/tot:.1%}  TB {b[2]/tot:.1%}  idle {b[8]/tot:.1%}  chunks {b[3]}  cycles/chunk {(b[0]+b[1]+b[2])/max(b[3],1):.0f}")
         print(f"   lanes in DC per chunk {b[4]/max(b[3],1):.1f}/32  TB trips/chunk {b[5]/max(b[3],1):.1f}  TB lane-steps/entry {b[6]/max(b[7],1):.1f}  TB entries {b[7]}  TB lane-util {b[6]/max(32*b[5],1):.1%}")
+    print(f"full warps: STD lane-chunks {buf[18]}  full-frame warp-chunks {buf[19]}  full-frame lane-chunks {buf[20]}")
+    print(f"coop: windows {buf[21]}  setup+DC cycles/window {buf[22]/max(buf[21],1):.0f}  TB cycles/window {buf[23]/max(buf[21],1):.0f}  mean D {buf[24]/max(buf[21],1):.1f}")

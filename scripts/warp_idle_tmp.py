@@ -1,0 +1,20 @@
+import ctypes as C, os, sys
+os.environ["SG_WARP_TIMES"] = "1"
+sys.path.insert(0, os.getcwd())
+import numpy as np
+import paper_2208_09985_b200 as sg
+from paper_2208_09985_b200 import _ffi
+batch = sg.synth_packed(int(sys.argv[1]) if len(sys.argv) > 1 else 3, 0, 100000)
+s = sg.Session(sg.AlignerConfig(W=64, O=24), batch)
+s.run(); ms, k1 = s.run()
+lib = _ffi.load()
+lib.sg_debug_warp_times.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+buf = (C.c_ulonglong * (3 * 8192))()
+n = lib.sg_debug_warp_times(buf, 8192)
+a = np.frombuffer(buf, dtype=np.uint64)[: 3 * n].reshape(n, 3).astype(np.int64); n = int((a[:, 0] > 0).sum()); a = a[:n]
+t0 = a[:, 0].min(); end = (a[:, 1] - t0) / 1e6
+wib = np.arange(n) % 8
+print("K1", k1, "warps", n)
+for name, sel in (("band", wib < 6), ("full", wib == 6), ("coop", wib == 7)):
+    e = end[sel]
+    print(name, "last-busy percentiles (ms):", " ".join(f"{x:.1f}" for x in np.percentile(e, [0, 10, 50, 90, 99, 100])))
