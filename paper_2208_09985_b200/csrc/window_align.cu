@@ -718,6 +718,34 @@ __device__ __forceinline__ int q_pop(uint32_t* q, int cap) {
     return static_cast<int>(v) - 1;
 }
 
+// Warp-aggregated pop for the calling lanes that `want` a pair: one CAS on the
+// head claims up to one entry per such lane (a per-lane CAS serialises every pop
+// on one address).
+__device__ __forceinline__ int q_pop_warp(uint32_t* q, int cap, bool want) {
+    const unsigned active = __activemask();
+    const unsigned wm = __ballot_sync(active, want);
+    if (!want) return -1;
+    const int leader = __ffs(wm) - 1;
+    const int lane = threadIdx.x & 31;
+    unsigned h = 0, take = 0;
+    if (lane == leader) {
+        h = *reinterpret_cast<volatile unsigned*>(q);
+        const unsigned t = *reinterpret_cast<volatile unsigned*>(q + 1);
+        const int avail = static_cast<int>(t - h);
+        take = avail > 0 ? min(static_cast<unsigned>(avail), static_cast<unsigned>(__popc(wm))) : 0u;
+        if (take && atomicCAS(q, h, h + take) != h) take = 0;  // lost the race: retry later
+    }
+    h = __shfl_sync(wm, h, leader);
+    take = __shfl_sync(wm, take, leader);
+    const unsigned rank = __popc(wm & ((1u << lane) - 1u));
+    if (rank >= take) return -1;
+    uint32_t* slot = q + 32 + (h + rank) % static_cast<unsigned>(cap);
+    uint32_t v;
+    while ((v = atomicExch(slot, 0u)) == 0u) __nanosleep(200);  // reserved, not yet written
+    __threadfence();
+    return static_cast<int>(v) - 1;
+}
+
 // The K1 window loop of one warp. BAND = true: the band frame (K1b) — windows
 // it cannot take (final windows, n_w < W, |m_w - n_w| > 30, D(0, 0) > 30) go
 // with the pair to a full-frame warp (P.mixed); a full-frame warp hands the
@@ -779,6 +807,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     int e_lo = 0, K0 = 0;  // band window: bit k <-> j = i + e_lo + k; (n_w, m_w) at bit K0
     int pass_win = 0;      // windows this warp completed for the pair (hand-back after one)
     int last_d = 0;        // D(0, 0) of the last window
+    unsigned long long ph_fresh_end = 0;  // diagnostics: when the fresh pairs ran out
     bool defer_now = false;
     bool std_win = false;  // full-frame warp, mixed: the window runs in the STD frame (m_w <= 31)
     int hand_to = 0;       // mixed: the role the pair goes to (0 band, 1 full frame, 2 cooperative)
@@ -1122,10 +1151,12 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         pair = -1;
         bool restore = false;
         if (P.mixed) {  // a pair handed over by the other frame first
-            pair = q_pop(BAND ? P.q_band : P.q_full, P.n_pairs);
-            if (pair < 0 && (!BAND || *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
-                                          static_cast<unsigned>(P.n_pairs)))
-                pair = q_pop(P.q_std, P.n_pairs);  // band warps: once no fresh pairs are left
+            pair = q_pop_warp(BAND ? P.q_band : P.q_full, P.n_pairs, true);
+            const bool fresh_left = BAND && *reinterpret_cast<const volatile unsigned*>(P.next_pair) <
+                                                static_cast<unsigned>(P.n_pairs);
+            // band warps take STD windows once no fresh pairs are left
+            const int sp = q_pop_warp(P.q_std, P.n_pairs, pair < 0 && !fresh_left);
+            if (pair < 0) pair = sp;
             restore = pair >= 0;
         }
         if (BAND || !P.mixed) {  // fresh pairs (warp-aggregated claim)
@@ -1141,6 +1172,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 base = __shfl_sync(wm, base, leader);
                 const int q = static_cast<int>(base + __popc(wm & ((1u << lane) - 1u)));
                 pair = q < P.n_pairs ? (P.order ? P.order[q] : q) : -1;
+                if (P.warp_times && pair < 0 && ph_fresh_end == 0)  // diagnostics
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ph_fresh_end));
             }
         }
         if (pair < 0) return;
@@ -1504,7 +1537,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned*>(&smid)));
         P.warp_times[dwarp * 3 + 1] = last_busy ? last_busy : t;
-        P.warp_times[dwarp * 3 + 2] = smid & 0xFFFFFFFFull;
+        P.warp_times[dwarp * 3 + 2] = __reduce_max_sync(kFull, static_cast<unsigned>(ph_fresh_end >> 20)) ;
     }
     if (P.phase_cycles) {
         ph_steps = __reduce_add_sync(kFull, static_cast<unsigned>(ph_steps));

@@ -4,7 +4,7 @@ sys.path.insert(0, os.getcwd())
 import numpy as np
 import paper_2208_09985_b200 as sg
 from paper_2208_09985_b200 import _ffi
-batch = sg.synth_packed(int(sys.argv[1]) if len(sys.argv) > 1 else 3, 0, 100000)
+batch = sg.synth_packed(int(sys.argv[1]) if len(sys.argv) > 1 else 3, 0, int(sys.argv[2]) if len(sys.argv) > 2 else 100000)
 s = sg.Session(sg.AlignerConfig(W=64, O=24), batch)
 s.run(); ms, k1 = s.run()
 lib = _ffi.load()
@@ -18,3 +18,6 @@ print("K1", k1, "warps", n)
 for name, sel in (("band", wib < 6), ("full", wib == 6), ("coop", wib == 7)):
     e = end[sel]
     print(name, "last-busy percentiles (ms):", " ".join(f"{x:.1f}" for x in np.percentile(e, [0, 10, 50, 90, 99, 100])))
+fe = a[:, 2][wib < 6]
+fe = fe[fe > 0]
+if len(fe): print("band fresh-exhausted (ms):", " ".join(f"{x:.1f}" for x in np.percentile(((fe << 20) - t0) / 1e6, [0, 50, 100])))
