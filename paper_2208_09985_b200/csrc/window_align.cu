@@ -1070,7 +1070,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             const bool std_ok = !fin && n_w == W && m_w <= 31;  // the STD frame takes it
             std_win = false;
             if (BAND) {
-                if (!band_ok) {
+                // a window the STD frame takes never runs in the band frame: STD is
+                // exact for every row (a band failure would otherwise come back here)
+                if (!band_ok || std_ok) {
                     // STD windows stay in this lane once no fresh pairs are left (the
                     // end of the batch: full-frame warps alone would drain them slowly)
                     if (std_ok && *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=

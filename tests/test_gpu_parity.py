@@ -305,3 +305,24 @@ def test_single_window_run_batch_and_tsv(gpu):
         a = O.align(O.encode(rec.text), O.encode(rec.pattern), dent=False, single_window=True,
                     k_single=64)
         assert po.distance == a.distance and sg.cigar_to_string(po.cigar) == a.cigar
+
+
+@pytest.mark.gpu
+def test_mixed_handoffs_terminate(gpu):
+    """K1 mixed: a window the band frame fails on (D > 30) must
+    not bounce between the warp roles. For W < 64 a window can be both band- and
+    STD-shaped; the W = 32 KATs hit that case (one of them looped for minutes
+    when the band frame could take such a window back)."""
+    import time
+    sg = gpu
+    pairs = G.kat_pairs()
+    rows = G.read_golden("kat_W32_O17.tsv")
+    codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
+                                     [sg.encode_sequence(pairs[r["id"]][1]) for r in rows])
+    sg.align_codes(_cfg(sg, 32, 17, 1, 1, 1), codes)  # warm-up
+    for _ in range(3):
+        t0 = time.time()
+        res = sg.align_codes(_cfg(sg, 32, 17, 1, 1, 1), codes)
+        assert time.time() - t0 < 5.0
+        for k, row in enumerate(rows):
+            _compare(res, k, row)
