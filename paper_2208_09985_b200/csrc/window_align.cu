@@ -20,10 +20,17 @@ template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4, MINB
 template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4, MINB = 3; };
 template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2, MINB = 1; };
 // DC chunks per state-machine iteration (traceback batching, see the main loop)
+// (band warps: their chunks cost a third of a full-frame chunk, so the traceback
+// and setup phases amortise over more of them; measured 2 / 3 / 4 / 6 / 8 on cfg3:
+// 4 is best)
 #ifndef SG_SUBCHUNKS
 #define SG_SUBCHUNKS 2
 #endif
+#ifndef SG_BAND_SUBCHUNKS
+#define SG_BAND_SUBCHUNKS 4
+#endif
 constexpr int kSubChunks = SG_SUBCHUNKS;
+constexpr int kBandSubChunks = SG_BAND_SUBCHUNKS;
 // (R = 4: sweep groups are aligned to 4-column text-code words; C % 4 == 0.)
 
 // Shared memory of one warp, in 32-bit words:
@@ -1309,7 +1316,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         // Up to kSubChunks chunks of R rows before the traceback phase, so
         // that more lanes reach it together; solved lanes sweep idle.
         bool solved = false;
-        for (int sub = 0; sub < kSubChunks; ++sub) {
+        for (int sub = 0; sub < (BAND ? kBandSubChunks : kSubChunks); ++sub) {
             const bool act = in_dc && !solved;
             if (sub > 0 && !__any_sync(kFull, act)) break;
             if constexpr (BAND) {
