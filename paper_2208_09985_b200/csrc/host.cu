@@ -196,7 +196,7 @@ struct DevState {
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
-    DevBuf q_band, q_full, q_coop, q_std, defer_count, resume_state;  // K1 mixed hand-over (§3.8)
+    DevBuf q_band, q_full, q_coop, q_std, defer_count, resume_state, u_list;  // K1 mixed hand-over (§3.8)
     long long grid = 0, lanes = 0;
 
     void init(int dev) {
@@ -215,7 +215,8 @@ struct DevState {
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
-                          &q_band, &q_full, &q_coop, &q_std, &defer_count, &resume_state})
+                          &q_band, &q_full, &q_coop, &q_std, &defer_count, &resume_state,
+                          &u_list})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
@@ -568,10 +569,10 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool str
     const sg_packed_pairs* in = s.in;
     const int64_t words = pp.word_hi - pp.word_lo;
     int64_t h2d_bytes = 0;
-    const size_t seq_bytes = 4 * static_cast<size_t>(words + 24);  // K1 reads up to 12 words past a start
+    const size_t seq_bytes = 4 * static_cast<size_t>(words + 48);  // K1 reads up to 12 words past a start, K0 35
     st.seq.ensure(seq_bytes);
     st.ready.ensure(4 * kChunks);
-    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 24, in->seq_words - pp.word_lo));
+    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 48, in->seq_words - pp.word_lo));
     st.chunk_words = std::max<int64_t>(1, (avail + kChunks - 1) / kChunks);
     cudaStream_t cs = streamed ? st.copy : st.stream;
     SG_CUDA_CHECK(cudaMemsetAsync(st.ready.p, 0, 4 * kChunks, st.stream));
@@ -770,10 +771,24 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_coop.p, 0, st.q_coop.cap, st.stream));
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_std.p, 0, st.q_std.cap, st.stream));
         SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_queue_init(
-            p.q_band, p.q_full, p.q_coop, p.q_std, p.remaining, static_cast<int>(n), st.stream)));
+            p.q_band, p.q_full, p.q_coop, p.q_std, p.remaining, static_cast<int>(n), nullptr,
+            st.stream)));
+        // K0 (§3.10): band warps leave unrelated pairs to a full-frame K1 after them
+        st.u_list.ensure(4 * n1);
+        SG_CUDA_CHECK(cudaMemsetAsync(st.defer_count.as<unsigned int>() + 8, 0, 4, st.stream));
+        p.u_list = st.u_list.as<int32_t>();
+        p.u_count = st.defer_count.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
-        launches += 2;
+        sgk::AlignParams pu = p;
+        pu.mixed = 0;
+        pu.u_list = nullptr;
+        pu.order = st.u_list.as<int32_t>();
+        pu.n_fresh = reinterpret_cast<const int32_t*>(p.u_count);
+        pu.next_pair = st.next_pair.as<unsigned int>() + 8;
+        SG_CUDA_CHECK(static_cast<cudaError_t>(
+            sgk::launch_window_align(rc.L, pu, static_cast<int>(grid), wpb, st.stream)));
+        launches += 3;
     } else if (n > 0) {
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             rc.wide ? sgk::launch_wide_align(p, static_cast<int>(grid), st.stream)

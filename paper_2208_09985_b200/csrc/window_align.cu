@@ -796,6 +796,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     const int W = P.W;
     const int step_limit = W - P.O;
     const int K = P.single ? P.k_single : W;  // edit budget: rows 0..K
+    // fresh pairs of this launch (a device count when a pre-pass split the batch)
+    const int n_fresh = P.n_fresh ? *P.n_fresh : P.n_pairs;
     // band pass: traceback-event columns, last exact row, shift multipliers
     const int cmax = BAND ? step_limit : C;
     const int band_last = min(K, band::kLastRow);
@@ -1083,7 +1085,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     // STD windows stay in this lane once no fresh pairs are left (the
                     // end of the batch: full-frame warps alone would drain them slowly)
                     if (std_ok && *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
-                                      static_cast<unsigned>(P.n_pairs)) {
+                                      static_cast<unsigned>(n_fresh)) {
                         std_win = true;
                     } else {
                         hand_to = wide_ok ? 2 : std_ok ? 3 : 1;
@@ -1113,6 +1115,14 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 
     // Hand the pair to the next pass (the other frame) before its current window.
     auto defer_pair = [&]() {
+        if (BAND && hand_to == 2 && nwin == 0 && P.u_list) {
+            // K0 (§3.10): the pair's first window already has D(0, 0) > 30: an
+            // unrelated pair (every window would go to a cooperative warp). The
+            // full-frame K1 after this kernel aligns it from the start.
+            P.u_list[atomicAdd(P.u_count, 1u)] = pair;
+            atomicSub(P.remaining, 1u);
+            return;
+        }
         P.distance[pair] = dist;
         P.windows[pair] = nwin;
         P.status[pair] = 0;
@@ -1162,7 +1172,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         if (P.mixed) {  // a pair handed over by the other frame first
             pair = q_pop_warp(BAND ? P.q_band : P.q_full, P.n_pairs, true);
             const bool fresh_left = BAND && *reinterpret_cast<const volatile unsigned*>(P.next_pair) <
-                                                static_cast<unsigned>(P.n_pairs);
+                                                static_cast<unsigned>(n_fresh);
             // band warps take STD windows once no fresh pairs are left
             const int sp = q_pop_warp(P.q_std, P.n_pairs, pair < 0 && !fresh_left);
             if (pair < 0) pair = sp;
@@ -1171,7 +1181,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         if (BAND || !P.mixed) {  // fresh pairs (warp-aggregated claim)
             const bool want = pair < 0 &&
                 (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.next_pair) <
-                                 static_cast<unsigned>(P.n_pairs));
+                                 static_cast<unsigned>(n_fresh));
             const unsigned active = __activemask();
             const unsigned wm = __ballot_sync(active, want);
             if (want) {
@@ -1180,7 +1190,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 if (lane == leader) base = atomicAdd(P.next_pair, static_cast<unsigned>(__popc(wm)));
                 base = __shfl_sync(wm, base, leader);
                 const int q = static_cast<int>(base + __popc(wm & ((1u << lane) - 1u)));
-                pair = q < P.n_pairs ? (P.order ? P.order[q] : q) : -1;
+                pair = q < n_fresh ? (P.order ? P.order[q] : q) : -1;
                 if (P.warp_times && pair < 0 && ph_fresh_end == 0)  // diagnostics
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ph_fresh_end));
             }
@@ -2003,7 +2013,8 @@ template <int LF> int launch_mixed_L(const AlignParams& p, int grid, void* strea
 }
 
 __global__ void k1_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop,
-                              uint32_t* q_std, unsigned* remaining, int n) {
+                              uint32_t* q_std, unsigned* remaining, int n, const int32_t* n_dev) {
+    if (n_dev) n = *n_dev;
     if (threadIdx.x < 32) {
         q_band[threadIdx.x] = 0u;
         q_full[threadIdx.x] = 0u;
@@ -2116,9 +2127,9 @@ int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream) {
 }
 
 int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint32_t* q_std,
-                      unsigned* remaining, int n, void* stream) {
+                      unsigned* remaining, int n, const int32_t* n_dev, void* stream) {
     k1_queue_init<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(q_band, q_full, q_coop, q_std,
-                                                                  remaining, n);
+                                                                  remaining, n, n_dev);
     return static_cast<int>(cudaGetLastError());
 }
 

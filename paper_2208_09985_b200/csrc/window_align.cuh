@@ -55,6 +55,7 @@ struct AlignParams {
     const uint8_t* has_n;     // per pair: any non-ACGT base (may be null)
     const int32_t* order;     // processing order (null = identity)
     int32_t n_pairs;
+    const int32_t* n_fresh;   // device count of the pairs in `order` to take (null: n_pairs)
     int32_t W, O, et, policy; // policy: 0 BaselineEdges, 1 SeneEntries, 2 DentTrimmed (counters)
     int32_t two;              // the constant 2 at run time (keeps the DP shift an IMAD)
     int32_t single;           // single-window mode (aligner.cpp:87-112)
@@ -83,6 +84,8 @@ struct AlignParams {
     uint32_t* q_std;          // pairs whose next window the STD frame takes (m_w <= 31)
     unsigned int* remaining;  // pairs not finished (warps exit at 0)
     int32_t* resume_state;    // [n_pairs][4]: toff, poff, cur_op | cur_len << 8, open word
+    int32_t* u_list;          // K0 (§3.10): unrelated pairs, left to a full-frame K1 launch
+    unsigned int* u_count;
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
@@ -117,7 +120,8 @@ int wide_max_blocks_per_sm();
 // (limb count LF); pairs move between them through device queues.
 int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream);
 int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint32_t* q_std,
-                      unsigned* remaining, int n, void* stream);
+                      unsigned* remaining, int n, const int32_t* n_dev, void* stream);
+
 int mixed_band_warps();
 int mixed_full_warps();
 int mixed_max_blocks_per_sm(int LF);
