@@ -424,6 +424,54 @@ struct Shard {
     int64_t lo, hi;
 };
 
+// Whether the mixed kernel (band frame first, §3.8-3.10) pays for this shard.
+// It wins when pairs are long (most windows are band windows: cfg3 1.50x, cfg4 up
+// to 2x) and loses when most windows are final / tail windows (cfg1, cfg2: short
+// reads, 4x) or when many pairs are unrelated (cfg5: they leave the band frame at
+// once). Decided per shard from the mean window count per pair and the unrelated
+// fraction of a strided sample of <= 256 pairs (exact 8-base blocks of the first
+// 512 text bases found in the pattern within +-16 diagonals: correlated reads give
+// ~17, unrelated ones ~0). Only the choice of kernel depends on it, never a result.
+uint32_t bases8(const uint32_t* seq, int64_t a) {  // 8 bases (16 bits) from base a on
+    const uint64_t w = static_cast<uint64_t>(seq[a >> 4]) | (static_cast<uint64_t>(seq[(a >> 4) + 1]) << 32);
+    return static_cast<uint32_t>(w >> (2 * (a & 15))) & 0xFFFFu;
+}
+
+bool pair_related(const sg_packed_pairs* in, int64_t k) {
+    const int64_t n = in->text_len[k], m = in->pat_len[k];
+    const int64_t len = std::min<int64_t>(std::min(n, m), 512);
+    if (len < 128) return true;
+    const int64_t ta = in->text_off[k], pa = in->pat_off[k];
+    int hits = 0;
+    for (int64_t b = 0; b + 8 <= len; b += 8) {
+        const uint32_t t = bases8(in->seq, ta + b);
+        for (int64_t dl = -16; dl <= 16; ++dl) {
+            const int64_t j = b + dl;
+            if (j < 0 || j + 8 > m) continue;
+            if (bases8(in->seq, pa + j) == t && ++hits >= 2) return true;
+        }
+    }
+    return false;
+}
+
+bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) {
+    if (const char* e = getenv("SG_FRAME")) return e[0] == 'b';  // experiments: band / full
+    const int64_t n = hi - lo;
+    if (n <= 0) return false;
+    double tot = 0;
+    for (int64_t k = lo; k < hi; ++k) tot += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
+    if (tot / static_cast<double>(n) / std::max(1, W - O) < 32.0) return false;
+    const int64_t samples = std::min<int64_t>(n, 256);
+    int tested = 0, unrelated = 0;
+    for (int64_t i = 0; i < samples; ++i) {
+        const int64_t k = lo + i * n / samples;
+        if (std::min(in->text_len[k], in->pat_len[k]) < 128) continue;
+        ++tested;
+        unrelated += !pair_related(in, k);
+    }
+    return unrelated * 20 <= tested;
+}
+
 // Host-side per-pair inputs of a shard: rebased offsets, lengths, bounds, order.
 struct ShardPrep {
     PinBuf text_off, pat_off, text_len, pat_len, has_n, bound_off, order;
@@ -979,12 +1027,14 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             mark("start");
             // streamed: the first round of lanes takes pairs from the front of memory
             const bool streamed = !getenv("SG_NO_STREAM");
-            const int64_t split = streamed ? pairs_in_flight(st, rcfg, s.hi - s.lo) : 0;
+            RunConfig rcs = rcfg;
+            rcs.band = rcfg.band && band_pays(in, s.lo, s.hi, rcfg.W, rcfg.O);
+            const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
             prep_shard(s, prep[d], mixed, split);
             mark("prep");
             o.h2d_bytes = upload_shard(st, s, prep[d], streamed);
             mark("upload");
-            o.launches = launch_shard(st, rcfg, prep[d]);
+            o.launches = launch_shard(st, rcs, prep[d]);
             mark("kernels");
             fetch_small(st, prep[d].n, o);
             mark("fetch");
@@ -1258,6 +1308,7 @@ int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int de
     try {
         s->cfg = *cfg;
         s->rc = run_config(cfg, pairs->n_pairs, pairs->text_len, pairs->pat_len);
+        s->rc.band = s->rc.band && band_pays(pairs, 0, pairs->n_pairs, s->rc.W, s->rc.O);
         s->st.init(device);
         s->n = pairs->n_pairs;
         bool mixed = false;

@@ -21,6 +21,16 @@ import oracle_ffi as O
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["auto", "band"])
+def frame(request, monkeypatch):
+    """Runs a test with the host's choice of K1 kernel and again with the mixed
+    band-frame kernel forced: small or short-read batches
+    otherwise go to the full-frame K1 (host.cu band_pays)."""
+    if request.param == "band":
+        monkeypatch.setenv("SG_FRAME", "band")
+    return request.param
+
+
 def _cfg(sg, W, Ov, s=1, d=1, e=1):
     return sg.AlignerConfig(W=W, O=Ov, sene=bool(s), dent=bool(d), early_termination=bool(e))
 
@@ -38,7 +48,7 @@ def _compare(res, k, row):
 
 
 @pytest.mark.parametrize("name,W,Ov,s,d,e", G.kat_files())
-def test_reference_kats(gpu, name, W, Ov, s, d, e):
+def test_reference_kats(gpu, frame, name, W, Ov, s, d, e):
     sg = gpu
     pairs = G.kat_pairs()
     rows = G.read_golden(name)
@@ -50,7 +60,7 @@ def test_reference_kats(gpu, name, W, Ov, s, d, e):
 
 
 @pytest.mark.parametrize("name,cfg,W,Ov,s,d,e", G.synth_files())
-def test_reference_configs(gpu, name, cfg, W, Ov, s, d, e):
+def test_reference_configs(gpu, frame, name, cfg, W, Ov, s, d, e):
     sg = gpu
     rows = G.read_golden(name)
     first = G.pair_index(rows[0]["id"])
@@ -96,7 +106,7 @@ CASES = [(1, 0), (2, 1), (3, 0), (5, 2), (7, 6), (16, 8), (31, 15), (32, 0), (32
 
 
 @pytest.mark.parametrize("W,Ov", CASES)
-def test_random_pairs_match_oracle(gpu, W, Ov):
+def test_random_pairs_match_oracle(gpu, frame, W, Ov):
     """Degenerate and multi-limb windows, N bases, unbalanced and tiny pairs
     (proj/tests/test_aligner.cpp:163-211, acceptance.cpp:244-254)."""
     sg = gpu
@@ -165,7 +175,7 @@ def test_wide_kernel_on_narrow_windows(gpu, monkeypatch, name):
             _compare(res, k, row)
 
 
-def test_pairs_within_one_window_are_exact(gpu):
+def test_pairs_within_one_window_are_exact(gpu, frame):
     """test_aligner.cpp:123-133: max(n, m) <= W is aligned exactly (Levenshtein)."""
     sg = gpu
     rng = random.Random(45)
@@ -184,7 +194,7 @@ def test_pairs_within_one_window_are_exact(gpu):
 
 
 @pytest.mark.parametrize("cfg_id", [1, 2, 3, 5])
-def test_full_size_properties(gpu, cfg_id):
+def test_full_size_properties(gpu, frame, cfg_id):
     """Every pair of the BASELINE config at full size: the CIGAR replays
     (validate_replay) and its edit count equals the distance; head/tail pairs
     equal the reference's golden vectors."""
@@ -203,7 +213,7 @@ def test_full_size_properties(gpu, cfg_id):
             _compare(res, G.pair_index(row["id"]), row)
 
 
-def test_cfg4_full_sweep_properties(gpu):
+def test_cfg4_full_sweep_properties(gpu, frame):
     sg = gpu
     codes = sg.synth_codes(4)
     pk = sg.pack(codes)
@@ -214,7 +224,7 @@ def test_cfg4_full_sweep_properties(gpu):
             _compare(res, G.pair_index(row["id"]), row)
 
 
-def test_sharding_and_determinism(gpu):
+def test_sharding_and_determinism(gpu, frame):
     """Output is byte-identical across runs and across shardings of the batch
     (acceptance.cpp:258-281 checks the same across thread counts)."""
     sg = gpu
@@ -308,13 +318,14 @@ def test_single_window_run_batch_and_tsv(gpu):
 
 
 @pytest.mark.gpu
-def test_mixed_handoffs_terminate(gpu):
+def test_mixed_handoffs_terminate(gpu, monkeypatch):
     """K1 mixed: a window the band frame fails on (D > 30) must
     not bounce between the warp roles. For W < 64 a window can be both band- and
     STD-shaped; the W = 32 KATs hit that case (one of them looped for minutes
     when the band frame could take such a window back)."""
     import time
     sg = gpu
+    monkeypatch.setenv("SG_FRAME", "band")
     pairs = G.kat_pairs()
     rows = G.read_golden("kat_W32_O17.tsv")
     codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
