@@ -701,9 +701,20 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
     return std::max(1LL, std::min(grid, max_grid));
 }
 
+// K1 mixed: band warps that take pairs (the whole-rounds sizing of k1_grid),
+// spread over one block per SM; the others exit at once.
+long long band_active_warps(const DevState& st, const RunConfig& rc, int64_t n) {
+    const long long max_warps = static_cast<long long>(st.sms) * sgk::mixed_band_warps();
+    const long long rounds = std::max(1LL, (static_cast<long long>(n) + 32 * max_warps - 1) / (32 * max_warps));
+    const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
+    long long w = (lanes_needed + 31) / 32;
+    if (const char* e = getenv("SG_BAND_WARPS")) w = atoll(e);  // experiments
+    return std::max(1LL, std::min(w, max_warps));
+}
+
 // Pairs K1 / K6 work on at once (lanes / warps of the grid).
 int64_t pairs_in_flight(const DevState& st, const RunConfig& rc, int64_t n) {
-    if (rc.band) return k1_grid(st, rc, n, true) * sgk::mixed_band_warps() * 32;
+    if (rc.band) return band_active_warps(st, rc, n) * 32;
     const long long g = k1_grid(st, rc, n);
     return rc.wide ? g * sgk::wide_warps_per_block() : g * sgk::k1_warps_per_block(rc.L) * 32;
 }
@@ -726,9 +737,10 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     const long long grid = k1_grid(st, rc, n);
     st.grid = grid;
     st.lanes = grid * wpb * (rc.wide ? 1 : 32);  // pairs in flight
-    const long long grid_band = rc.band ? k1_grid(st, rc, n, true) : 0;
+    const long long band_warps = rc.band ? band_active_warps(st, rc, n) : 0;
+    const long long grid_band = rc.band ? std::min<long long>(st.sms, band_warps) : 0;
     if (rc.band) {
-        st.lanes = grid_band * sgk::mixed_band_warps() * 32;
+        st.lanes = band_warps * 32;
         st.q_band.ensure(4 * (n1 + 32));
         st.q_full.ensure(4 * (n1 + 32));
         st.q_coop.ensure(4 * (n1 + 32));
@@ -788,7 +800,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
             SG_CUDA_CHECK(cudaMemsetAsync(wbuf, 0, 8 * 3 * 8192, st.stream));
             p.warp_times = wbuf;
             g_warp_times = wbuf;
-            g_warp_count = static_cast<int>(rc.band ? grid_band * 8 : grid * wpb);
+            g_warp_count = static_cast<int>(rc.band ? grid_band * 9 : grid * wpb);
         }
     }
     if (const char* e = getenv("SG_PHASE_CYCLES")) {
@@ -808,6 +820,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         // cannot take move with their pair to the block's full-frame warps and
         // back (§3.8)
         p.mixed = 1;
+        p.band_active = static_cast<int32_t>(band_warps);
         p.q_band = st.q_band.as<uint32_t>();
         p.q_full = st.q_full.as<uint32_t>();
         p.q_coop = st.q_coop.as<uint32_t>();
@@ -828,7 +841,15 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         p.u_count = st.defer_count.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
+        if (getenv("SG_BAND_DEBUG")) {  // development aid: how many pairs K0 diverted
+            unsigned cnt = 0;
+            SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+            SG_CUDA_CHECK(cudaMemcpy(&cnt, p.u_count, 4, cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "[sg band] %u of %lld pairs to the full-frame K1\n", cnt,
+                         static_cast<long long>(n));
+        }
         sgk::AlignParams pu = p;
+        pu.warp_times = nullptr;
         pu.mixed = 0;
         pu.u_list = nullptr;
         pu.order = st.u_list.as<int32_t>();

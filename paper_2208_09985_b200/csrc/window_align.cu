@@ -524,8 +524,9 @@ constexpr int R = 4;
 constexpr int WMAX = 64;              // widest band-mode window (columns)
 constexpr int CMAX = 40;              // traceback-event columns (W - O <= 40)
 constexpr int kLastRow = 30;          // rows 0..30 are exact
-constexpr int WARPS = 6;              // band warps per block (one block per SM) ...
-constexpr int FWARPS = 1;             // ... plus a full-frame warp (K1 mixed)
+constexpr int WARPS = 7;              // band warps per block (one block per SM) ...
+constexpr int FWARPS = 0;             // (no full-frame warp in K1 mixed) ...
+constexpr int CWARPS = 2;             // ... plus cooperative warps
 constexpr int kBackRow = 24;          // a full-frame warp hands a pair back after D(0,0) <= 24
 // per-warp shared memory, in 32-bit words:
 //   eqp [WMAX + 4][32] uint2  (EQ_i, parked row) of column i at slot i + 4
@@ -723,6 +724,26 @@ __device__ __forceinline__ int q_pop(uint32_t* q, int cap) {
     while ((v = atomicExch(slot, 0u)) == 0u) __nanosleep(200);  // reserved, not yet written
     __threadfence();
     return static_cast<int>(v) - 1;
+}
+
+// Pops up to `maxn` entries with one CAS (a cooperative warp takes several when
+// the queue is long: one CAS per pair serialises the pops on one L2 line when
+// every pair hands its last window over at once). Single-thread.
+__device__ __forceinline__ int q_pop_n(uint32_t* q, int cap, int maxn, int* out) {
+    const unsigned h = *reinterpret_cast<volatile unsigned*>(q);
+    const unsigned t = *reinterpret_cast<volatile unsigned*>(q + 1);
+    const int avail = static_cast<int>(t - h);
+    if (avail <= 0) return 0;
+    const int take = min(maxn, max(1, avail / 32));
+    if (atomicCAS(q, h, h + static_cast<unsigned>(take)) != h) return 0;
+    for (int k = 0; k < take; ++k) {
+        uint32_t* slot = q + 32 + (h + k) % static_cast<unsigned>(cap);
+        uint32_t v;
+        while ((v = atomicExch(slot, 0u)) == 0u) __nanosleep(200);
+        out[k] = static_cast<int>(v) - 1;
+    }
+    __threadfence();
+    return take;
 }
 
 // Warp-aggregated pop for the calling lanes that `want` a pair: one CAS on the
@@ -1088,7 +1109,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                                       static_cast<unsigned>(n_fresh)) {
                         std_win = true;
                     } else {
-                        hand_to = wide_ok ? 2 : std_ok ? 3 : 1;
+                        hand_to = std_ok ? 3 : 2;  // STD queue (band warps drain it at the end) or cooperative
                         return 2;
                     }
                 } else {
@@ -1625,9 +1646,17 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
         P.warp_times[dwarp * 3] = t;
         P.warp_times[dwarp * 3 + 1] = t;
     }
+    int held[8], nheld = 0, next_held = 0;  // lane 0: pairs taken in one pop
     for (;;) {
         int pair = -1;
-        if (lane == 0) pair = q_pop(P.q_coop, P.n_pairs);
+        if (lane == 0) {
+            if (next_held == nheld) {
+                next_held = 0;
+                nheld = q_pop_n(P.q_coop, P.n_pairs, 8, held);
+                if (nheld == 0) nheld = q_pop_n(P.q_std, P.n_pairs, 8, held);
+            }
+            if (next_held < nheld) pair = held[next_held++];
+        }
         pair = __shfl_sync(kFull, pair, 0);
         if (pair < 0) {
             if (*reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
@@ -1696,7 +1725,9 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
             const int n_w = min(W, n_rem), m_w = min(W, m_rem), dl = m_w - n_w;
             const bool band_ok = !fin && n_w == W && dl <= band::kLastRow && dl >= -band::kLastRow;
             if (pass_win > 0 && band_ok && last_d <= band::kBackRow) { hand = 0; break; }
-            if (fin || n_w != W || m_w < 32) { hand = !fin && n_w == W ? 3 : 1; break; }
+            // this warp takes every other window: final ones (traceback to the
+            // end, events of every column) and the tails of the STD queue too
+            const int lim = fin ? 0x3FFFFFFF : step_limit, cap = fin ? n_w : step_limit;
             const long long cw0 = clock64();
             // ---- staging: the window's packed text / pattern (bases 16k.. in word k) and N bits
             {
@@ -1779,7 +1810,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                         // r + 1 reaches a column one step after lane r, so the
                         // read-modify-write is race-free
                         const uint64_t x = mt & ~nc, y = v & ~nc;
-                        const int es = act && col < step_limit ? col : 64;
+                        const int es = act && col < cap ? col : 64;
                         uint4 o = xys[es];
                         o.x |= static_cast<uint32_t>(x);
                         o.y |= static_cast<uint32_t>(x >> 32);
@@ -1805,7 +1836,8 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
             // reference counters of the window (dp.cpp:23-37,58-75,225-228)
             {
                 const int rows_ref = P.et ? found + 1 : K + 1;
-                const int pol = P.policy;
+                int pol = P.policy;
+                if (fin && pol == 2) pol = 1;  // final window: DENT -> SENE (aligner.cpp:79)
                 int keep_cols = n_w + 1, keep_bits = m_w;
                 if (pol == 2) {
                     keep_cols = min(n_w, step_limit) + 1;
@@ -1822,7 +1854,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
             int i = 0, j = 0, d = found, steps = 0;
             unsigned reads = 0;
             for (;;) {
-                int rem = step_limit - steps;
+                int rem = lim - steps;
                 if (rem == 0 || i == n_w || j == m_w) break;
                 int run;
                 {   // matching bases from (i, j) on
@@ -1865,7 +1897,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                 emit(op, 1);
             }
             {   // one side consumed: a single run of indels (traceback.cpp:76-86)
-                const int rem = step_limit - steps;
+                const int rem = lim - steps;
                 if (rem > 0 && !(i == n_w && j == m_w) && (i == n_w || j == m_w)) {
                     const int op = i == n_w ? 2 : 3;
                     const int left = i == n_w ? m_w - j : n_w - i;
@@ -1873,10 +1905,12 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                     const int k = min(rem, left);
                     i += op != 2 ? k : 0;
                     j += op != 3 ? k : 0;
+                    d -= k;
                     dist += k;
                     emit(op, k);
                 }
             }
+            if (fin && d != 0 && status == 0) status = kStInternal | kDetLeftover;  // traceback.cpp:110-111
             cn[2] += reads;
             toff += i;
             poff += j;
@@ -1965,21 +1999,24 @@ template <int LF> __host__ __device__ constexpr int mixed_full_words() {
 }
 template <int LF> __host__ __device__ constexpr int mixed_block_words() {
     return band::WARPS * k1_warp_words<2, true>() + band::FWARPS * mixed_full_words<LF>() +
-           coop::kWords;
+           band::CWARPS * coop::kWords;
 }
-constexpr int kMixedWarps = band::WARPS + band::FWARPS + 1;  // + one cooperative warp
+constexpr int kMixedWarps = band::WARPS + band::FWARPS + band::CWARPS;
 template <int LF>
 __global__ void __launch_bounds__(32 * kMixedWarps, 1)
     k1_mixed(const __grid_constant__ AlignParams P) {
     extern __shared__ uint32_t smem[];
     const int wib = threadIdx.x >> 5;
-    if (wib == kMixedWarps - 1) {
+    if (wib >= band::WARPS + band::FWARPS) {
         coop_body(P, smem + band::WARPS * k1_warp_words<2, true>() +
-                         band::FWARPS * mixed_full_words<LF>());
+                         band::FWARPS * mixed_full_words<LF>() +
+                         (wib - band::WARPS - band::FWARPS) * coop::kWords);
     } else if (wib < band::WARPS) {
+        if (wib * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x) >= P.band_active)
+            return;  // whole-rounds sizing: fewer band warps than slots, spread over the SMs
         k1_body<2, true>(P, smem + wib * k1_warp_words<2, true>(),
                          static_cast<long long>(blockIdx.x) * band::WARPS + wib, nullptr, nullptr);
-    } else {
+    } else if constexpr (band::FWARPS > 0) {
         const int fw = wib - band::WARPS;
         uint32_t* const base = smem + band::WARPS * k1_warp_words<2, true>() + fw * mixed_full_words<LF>();
         k1_body<LF, false>(P, base, static_cast<long long>(blockIdx.x) * band::FWARPS + fw,
