@@ -701,13 +701,15 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
     return std::max(1LL, std::min(grid, max_grid));
 }
 
-// K1 mixed: band warps that take pairs (the whole-rounds sizing of k1_grid),
-// spread over one block per SM; the others exit at once.
+// K1 mixed: band warps that take pairs, spread over one block per SM; the others
+// exit at once. Every slot when there are more pairs than lanes: unlike the
+// full-frame kernel, whole rounds do not pay here (cfg3 100k: 3.02 rounds on all
+// 1036 warps 28.7 ms, 4 whole rounds on 782 warps 33.7 ms) — the last pairs run
+// on nearly idle SMs and hand their tails to the cooperative warps.
 long long band_active_warps(const DevState& st, const RunConfig& rc, int64_t n) {
+    (void)rc;
     const long long max_warps = static_cast<long long>(st.sms) * sgk::mixed_band_warps();
-    const long long rounds = std::max(1LL, (static_cast<long long>(n) + 32 * max_warps - 1) / (32 * max_warps));
-    const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
-    long long w = (lanes_needed + 31) / 32;
+    long long w = (static_cast<long long>(n) + 31) / 32;
     if (const char* e = getenv("SG_BAND_WARPS")) w = atoll(e);  // experiments
     return std::max(1LL, std::min(w, max_warps));
 }
