@@ -683,14 +683,15 @@ __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K
 #pragma unroll
     for (int U = 0; U < 4; ++U) F[U] = M.eqp[(W - 1 - U + 4) * 32];
     band_group<kBFill, STD>(S, F, M, W - 1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    for (int col_top = W - 5; col_top >= 3; col_top -= 4) {
-        if (col_top - 3 >= C)
-            band_group<kBOut, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-        else if (col_top + 3 < C)
-            band_group<kBIn, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-        else
-            band_group<kBMix, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    }
+    // steady groups in three runs (no per-group mode test): right of the event
+    // columns, the one or two groups that straddle column C, inside them
+    int col_top = W - 5;
+    for (; col_top >= 3 && col_top - 3 >= C; col_top -= 4)
+        band_group<kBOut, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    for (; col_top >= 3 && col_top + 3 >= C; col_top -= 4)
+        band_group<kBMix, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    for (; col_top >= 3; col_top -= 4)
+        band_group<kBIn, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
     band_group<kBDrain, STD>(S, F, M, -1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
     int fr = -1;
 #pragma unroll
