@@ -989,9 +989,13 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 phi[h] = compress_stride<2>((pw[2 * h] >> 1) & 0x55555555u) |
                          (compress_stride<2>((pw[2 * h + 1] >> 1) & 0x55555555u) << 16);
             }
-            uint2* const lut = bmem.xy;
+            // per code c (and c | 4 for a non-ACGT text base: no match), the plane
+            // over j in [e_lo, e_lo + 96) as (s0, s1), (s1, s2) pairs: column i's
+            // window is then bits [i, i + 32) of s, a static funnel shift
+            uint2* const lut = bmem.xy;  // entry (2c + w) at lut[(2c + w) * 32], c < 8
+            const int ob = e_lo + 32;    // j = e_lo is bit ob of the [-32, 96) plane
 #pragma unroll
-            for (int c = 0; c < 5; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 uint32_t q[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -999,16 +1003,21 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     const uint32_t valid = (vb == 32 ? ~0u : ((1u << vb) - 1u)) & ~pn[h];
                     const uint32_t lo = plo[h], hi = phi[h];
                     const uint32_t e = c == 0 ? ~lo & ~hi : c == 1 ? lo & ~hi
-                                       : c == 2 ? ~lo & hi : c == 3 ? lo & hi : 0u;
+                                       : c == 2 ? ~lo & hi : lo & hi;
                     q[h + 1] = e & valid;  // j >= m_w and pattern N: no match
                 }
-#pragma unroll
-                for (int w = 0; w < 3; ++w) lut[(3 * c + w) * 32] = make_uint2(q[w], q[w + 1]);
+                const uint32_t s0 = __funnelshift_r(q[0], q[1], ob);
+                const uint32_t s1 = __funnelshift_r(q[1], q[2], ob);
+                const uint32_t s2 = __funnelshift_r(q[2], q[3], ob);
+                lut[(2 * c) * 32] = make_uint2(s0, s1);
+                lut[(2 * c + 1) * 32] = make_uint2(s1, s2);
+                lut[(2 * c + 8) * 32] = make_uint2(0u, 0u);  // code c | 4
+                lut[(2 * c + 9) * 32] = make_uint2(0u, 0u);
             }
-            // EQ_i of every column: bits j in [i + e_lo, i + e_lo + 32) of plane t_i;
-            // the parked row starts as row -1 (all zeros)
-            const int ob = e_lo + 32;  // bit offset of column 0's window from j = -32
-            for (int k = 0; 16 * k < n_w; ++k) {
+            // EQ_i of every column (the parked row starts as row -1: zeros)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (16 * k >= n_w) break;
                 const int bt = t_sh + 16 * k;
                 const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
                                                        sq_t[((bt >> 4) + 1) * 32 + lane],
@@ -1017,11 +1026,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int i = 16 * k + u;
-                    int code = static_cast<int>((tword >> (2 * u)) & 3u);
-                    if (hasn && ((tnw >> u) & 1u)) code = 4;
-                    const int o = ob + i;
-                    const uint2 pr = lut[(3 * code + (o >> 5)) * 32];
-                    bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, o & 31), 0u);
+                    const uint32_t code = ((tword >> (2 * u)) & 3u) | (((tnw >> u) & 1u) << 2);
+                    const uint2 pr = lut[(2 * code + (i >> 5)) * 32];
+                    bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, i & 31), 0u);
                 }
             }
 #pragma unroll
