@@ -461,6 +461,7 @@ bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) 
     double tot = 0;
     for (int64_t k = lo; k < hi; ++k) tot += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
     if (tot / static_cast<double>(n) / std::max(1, W - O) < 32.0) return false;
+    if (W <= 32) return false;  // one-limb full frame: no cheaper than the band (cfg4 W=32: 6.7 vs 7.0 ms)
     const int64_t samples = std::min<int64_t>(n, 256);
     int tested = 0, unrelated = 0;
     for (int64_t i = 0; i < samples; ++i) {
