@@ -172,6 +172,10 @@ int sg_session_run(sg_session* s, float* device_ms, float* k1_ms);
 int sg_session_fetch(sg_session* s, sg_results* out);
 /* Per-session facts for the roofline: resident lanes, SMs, K1 launches. */
 int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* limbs);
+/* Which K1 the session runs: 0 the full-frame kernel, 1 the mixed
+ * band / cooperative kernel, 2 the wide-window kernel K6. Diagnostics; no reference
+ * counterpart. */
+int sg_session_kernel(const sg_session* s);
 void sg_session_destroy(sg_session* s);
 
 /* Measured integer-ALU issue rate of `device` (LOP3 lane-ops per clock per SM,

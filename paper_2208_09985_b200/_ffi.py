@@ -22,7 +22,7 @@ EXPORTS = (
     "sg_validate_config", "sg_align_batch", "sg_align_packed", "sg_results_free",
     "sg_cigar_string", "sg_cigar_runs", "sg_pack", "sg_packed_free",
     "sg_last_transfer_bytes", "sg_session_create", "sg_session_run", "sg_session_fetch",
-    "sg_session_info", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
+    "sg_session_info", "sg_session_kernel", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
     "sg_pairs_free", "sg_alu_peak", "sg_read_pairs", "sg_pair_file_free", "sg_write_results",
     "sg_global_align", "sg_scoring_default", "sg_score_cigar", "sg_worst_quantile", "sg_sweep",
     "sg_sweep_format",
@@ -124,6 +124,8 @@ def load(build_if_missing: bool = True):
     L.sg_session_run.argtypes = [C.c_void_p, P(C.c_float), P(C.c_float)]
     L.sg_session_fetch.argtypes = [C.c_void_p, P(SgResults)]
     L.sg_session_info.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int32), P(C.c_int32)]
+    L.sg_session_kernel.argtypes = [C.c_void_p]
+    L.sg_session_kernel.restype = C.c_int
     L.sg_session_destroy.argtypes = [C.c_void_p]
     L.sg_session_destroy.restype = None
     L.sg_synth_packed.argtypes = [C.c_int, C.c_int64, C.c_int64, P(SgPackedPairs)]

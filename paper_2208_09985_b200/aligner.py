@@ -482,7 +482,8 @@ class Session:
     def info(self):
         lanes, sms, limbs = C.c_int64(), C.c_int32(), C.c_int32()
         _ffi.load().sg_session_info(self._h, C.byref(lanes), C.byref(sms), C.byref(limbs))
-        return {"lanes": lanes.value, "sms": sms.value, "limbs": limbs.value}
+        kernel = ("full", "mixed", "wide")[_ffi.load().sg_session_kernel(self._h)]
+        return {"lanes": lanes.value, "sms": sms.value, "limbs": limbs.value, "kernel": kernel}
 
     def close(self):
         if self._h:

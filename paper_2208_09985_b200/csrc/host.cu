@@ -1400,6 +1400,8 @@ int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* 
     return SG_OK;
 }
 
+int sg_session_kernel(const sg_session* s) { return s->rc.wide ? 2 : s->rc.band ? 1 : 0; }
+
 void sg_session_destroy(sg_session* s) { delete s; }
 
 /* Diagnostics: per-phase SM cycles summed over warps of the last run with

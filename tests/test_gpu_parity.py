@@ -337,3 +337,19 @@ def test_mixed_handoffs_terminate(gpu, monkeypatch):
         assert time.time() - t0 < 5.0
         for k, row in enumerate(rows):
             _compare(res, k, row)
+
+
+@pytest.mark.gpu
+def test_kernel_choice(gpu):
+    """host.cu band_pays: long correlated reads run the mixed
+    kernel; short reads, W <= 32 and batches with many unrelated pairs the full
+    frame; W > 128 the wide kernel."""
+    sg = gpu
+    def kernel(cfg_id, count, W, Ov):
+        return sg.Session(sg.AlignerConfig(W=W, O=Ov), sg.synth_packed(cfg_id, 0, count)).info()["kernel"]
+    assert kernel(3, 2000, 64, 24) == "mixed"
+    assert kernel(4, 500, 64, 33) == "mixed"
+    assert kernel(4, 500, 32, 12) == "full"
+    assert kernel(2, 2000, 64, 24) == "full"
+    assert kernel(5, 2000, 64, 24) == "full"
+    assert kernel(4, 200, 256, 96) == "wide"
