@@ -527,7 +527,14 @@ constexpr int kLastRow = 30;          // rows 0..30 are exact
 constexpr int WARPS = 7;              // band warps per block (one block per SM) ...
 constexpr int FWARPS = 0;             // (no full-frame warp in K1 mixed) ...
 constexpr int CWARPS = 2;             // ... plus cooperative warps
-constexpr int kBackRow = 24;          // a full-frame warp hands a pair back after D(0,0) <= 24
+#ifndef SG_BACK_ROW
+#define SG_BACK_ROW 24
+#endif
+#ifndef SG_COOP_SLEEP
+#define SG_COOP_SLEEP 4000
+#endif
+constexpr int kBackRow = SG_BACK_ROW;  // a pair goes back to the band warps after D(0,0) <= 24
+constexpr int kCoopSleep = SG_COOP_SLEEP;  // ns between an idle cooperative warp's polls
 // per-warp shared memory, in 32-bit words:
 //   eqp [WMAX + 4][32] uint2  (EQ_i, parked row) of column i at slot i + 4
 //   xy  [CMAX + 1][32] uint2  events X / Y; column C (runtime) is the dummy
@@ -1668,7 +1675,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
         pair = __shfl_sync(kFull, pair, 0);
         if (pair < 0) {
             if (*reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
-            __nanosleep(4000);
+            __nanosleep(band::kCoopSleep);
             continue;
         }
         // ---- restore the pair (every lane holds the same state; lane 0 writes)
