@@ -429,9 +429,9 @@ struct Shard {
 // to 2x) and loses when most windows are final / tail windows (cfg1, cfg2: short
 // reads, 4x) or when many pairs are unrelated (cfg5: they leave the band frame at
 // once). Decided per shard from the mean window count per pair and the unrelated
-// fraction of a strided sample of <= 256 pairs (exact 8-base blocks of the first
-// 512 text bases found in the pattern within +-16 diagonals: correlated reads give
-// ~17, unrelated ones ~0). Only the choice of kernel depends on it, never a result.
+// fraction of a strided sample of <= 64 pairs (exact 8-base blocks of the first
+// 256 text bases found in the pattern within +-16 diagonals: correlated reads give
+// ~8, unrelated ones ~0.02; the sample costs ~0.1 ms of host time per call). Only the choice of kernel depends on it, never a result.
 uint32_t bases8(const uint32_t* seq, int64_t a) {  // 8 bases (16 bits) from base a on
     const uint64_t w = static_cast<uint64_t>(seq[a >> 4]) | (static_cast<uint64_t>(seq[(a >> 4) + 1]) << 32);
     return static_cast<uint32_t>(w >> (2 * (a & 15))) & 0xFFFFu;
@@ -439,7 +439,7 @@ uint32_t bases8(const uint32_t* seq, int64_t a) {  // 8 bases (16 bits) from bas
 
 bool pair_related(const sg_packed_pairs* in, int64_t k) {
     const int64_t n = in->text_len[k], m = in->pat_len[k];
-    const int64_t len = std::min<int64_t>(std::min(n, m), 512);
+    const int64_t len = std::min<int64_t>(std::min(n, m), 256);
     if (len < 128) return true;
     const int64_t ta = in->text_off[k], pa = in->pat_off[k];
     int hits = 0;
@@ -462,7 +462,7 @@ bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) 
     for (int64_t k = lo; k < hi; ++k) tot += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
     if (tot / static_cast<double>(n) / std::max(1, W - O) < 32.0) return false;
     if (W <= 32) return false;  // one-limb full frame: no cheaper than the band (cfg4 W=32: 6.7 vs 7.0 ms)
-    const int64_t samples = std::min<int64_t>(n, 256);
+    const int64_t samples = std::min<int64_t>(n, 64);
     int tested = 0, unrelated = 0;
     for (int64_t i = 0; i < samples; ++i) {
         const int64_t k = lo + i * n / samples;
@@ -491,18 +491,27 @@ bool any_bits(const uint32_t* m, int64_t base, int64_t len) {
     return false;
 }
 
-void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split = 0) {
+// Packed words a shard's pairs use: [lo, hi), lo even (the N mask stays 32-bit
+// aligned after rebasing).
+void shard_words(const Shard& s, int64_t* lo, int64_t* hi) {
     const sg_packed_pairs* in = s.in;
-    const int64_t n = s.hi - s.lo;
-    pp.n = n;
     int64_t wlo = INT64_MAX, whi = 0;
     for (int64_t k = s.lo; k < s.hi; ++k) {
         wlo = std::min({wlo, in->text_off[k] >> 4, in->pat_off[k] >> 4});
         whi = std::max({whi, (in->text_off[k] + in->text_len[k] + 15) >> 4,
                         (in->pat_off[k] + in->pat_len[k] + 15) >> 4});
     }
-    if (n == 0) wlo = whi = 0;
-    wlo &= ~int64_t{1};  // even word: the N mask stays 32-bit aligned after rebasing
+    if (s.hi <= s.lo) wlo = whi = 0;
+    *lo = wlo & ~int64_t{1};
+    *hi = whi;
+}
+
+void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split = 0) {
+    const sg_packed_pairs* in = s.in;
+    const int64_t n = s.hi - s.lo;
+    pp.n = n;
+    int64_t wlo = 0, whi = 0;
+    shard_words(s, &wlo, &whi);
     pp.word_lo = wlo;
     pp.word_hi = whi;
     const int64_t rebase = wlo * 16;
@@ -613,15 +622,16 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
 // (K1 fetch). Otherwise (sessions) everything is copied and flagged up front.
 constexpr int kChunks = 16;
 
-int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool streamed = false) {
-    const int64_t n = pp.n;
+// The sequence words (the bulk of the H2D), issued before the host prepares the
+// per-pair arrays so that they arrive earlier (one-shot calls stream them, §1).
+int64_t upload_seq(DevState& st, const Shard& s, int64_t word_lo, int64_t word_hi, bool streamed) {
     const sg_packed_pairs* in = s.in;
-    const int64_t words = pp.word_hi - pp.word_lo;
+    const int64_t words = word_hi - word_lo;
     int64_t h2d_bytes = 0;
     const size_t seq_bytes = 4 * static_cast<size_t>(words + 48);  // K1 reads up to 12 words past a start, K0 35
     st.seq.ensure(seq_bytes);
     st.ready.ensure(4 * kChunks);
-    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 48, in->seq_words - pp.word_lo));
+    const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 48, in->seq_words - word_lo));
     st.chunk_words = std::max<int64_t>(1, (avail + kChunks - 1) / kChunks);
     cudaStream_t cs = streamed ? st.copy : st.stream;
     SG_CUDA_CHECK(cudaMemsetAsync(st.ready.p, 0, 4 * kChunks, st.stream));
@@ -636,12 +646,21 @@ int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool str
         const int64_t lo = std::min<int64_t>(avail, c * st.chunk_words);
         const int64_t hi = std::min<int64_t>(avail, lo + st.chunk_words);
         if (hi > lo) {
-            SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.as<uint32_t>() + lo, in->seq + pp.word_lo + lo,
+            SG_CUDA_CHECK(cudaMemcpyAsync(st.seq.as<uint32_t>() + lo, in->seq + word_lo + lo,
                                           4 * static_cast<size_t>(hi - lo), cudaMemcpyHostToDevice, cs));
             h2d_bytes += 4 * (hi - lo);
         }
         SG_CUDA_CHECK(cudaMemsetAsync(st.ready.as<uint32_t>() + c, 1, 4, cs));
     }
+    return h2d_bytes;
+}
+
+int64_t upload_shard(DevState& st, const Shard& s, const ShardPrep& pp, bool streamed = false,
+                     bool seq_done = false) {
+    const int64_t n = pp.n;
+    const sg_packed_pairs* in = s.in;
+    const int64_t words = pp.word_hi - pp.word_lo;
+    int64_t h2d_bytes = seq_done ? 0 : upload_seq(st, s, pp.word_lo, pp.word_hi, streamed);
     if (pp.any_n) {
         const int64_t mlo = pp.word_lo / 2;
         const int64_t mwords = (words + 1) / 2 + 4;
@@ -1051,12 +1070,16 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             mark("start");
             // streamed: the first round of lanes takes pairs from the front of memory
             const bool streamed = !getenv("SG_NO_STREAM");
+            // the sequence words first: their copy overlaps the host prep below
+            int64_t wlo = 0, whi = 0;
+            shard_words(s, &wlo, &whi);
+            o.h2d_bytes = upload_seq(st, s, wlo, whi, streamed);
             RunConfig rcs = rcfg;
             rcs.band = rcfg.band && band_pays(in, s.lo, s.hi, rcfg.W, rcfg.O);
             const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
             prep_shard(s, prep[d], mixed, split);
             mark("prep");
-            o.h2d_bytes = upload_shard(st, s, prep[d], streamed);
+            o.h2d_bytes += upload_shard(st, s, prep[d], streamed, true);
             mark("upload");
             o.launches = launch_shard(st, rcs, prep[d]);
             mark("kernels");
