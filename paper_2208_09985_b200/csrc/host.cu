@@ -196,7 +196,9 @@ struct DevState {
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
-    DevBuf q_band, q_full, q_coop, q_std, defer_count, resume_state, u_list;  // K1 mixed hand-over (§3.8)
+    // K1 mixed (§3.8-3.10): hand-over queues, counters (remaining pairs, K0 count),
+    // the handed pairs' state, K0's list of unrelated pairs
+    DevBuf q_band, q_full, q_coop, q_std, mixed_ctr, resume_state, u_list;
     long long grid = 0, lanes = 0;
 
     void init(int dev) {
@@ -215,7 +217,7 @@ struct DevState {
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
-                          &q_band, &q_full, &q_coop, &q_std, &defer_count, &resume_state,
+                          &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state,
                           &u_list})
             b->release();
         if (copy) cudaStreamDestroy(copy);
@@ -767,7 +769,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         st.q_full.ensure(4 * (n1 + 32));
         st.q_coop.ensure(4 * (n1 + 32));
         st.q_std.ensure(4 * (n1 + 32));
-        st.defer_count.ensure(64);
+        st.mixed_ctr.ensure(64);
         st.resume_state.ensure(16 * n1);
     }
     st.bnd.ensure(rc.wide ? static_cast<size_t>(sgk::wide_warp_words(rc.wcap)) * 4 * grid * wpb
@@ -847,7 +849,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         p.q_full = st.q_full.as<uint32_t>();
         p.q_coop = st.q_coop.as<uint32_t>();
         p.q_std = st.q_std.as<uint32_t>();
-        p.remaining = st.defer_count.as<unsigned int>();
+        p.remaining = st.mixed_ctr.as<unsigned int>();
         p.resume_state = st.resume_state.as<int32_t>();
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_band.p, 0, st.q_band.cap, st.stream));
         SG_CUDA_CHECK(cudaMemsetAsync(st.q_full.p, 0, st.q_full.cap, st.stream));
@@ -858,9 +860,9 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
             st.stream)));
         // K0 (§3.10): band warps leave unrelated pairs to a full-frame K1 after them
         st.u_list.ensure(4 * n1);
-        SG_CUDA_CHECK(cudaMemsetAsync(st.defer_count.as<unsigned int>() + 8, 0, 4, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.mixed_ctr.as<unsigned int>() + 8, 0, 4, st.stream));
         p.u_list = st.u_list.as<int32_t>();
-        p.u_count = st.defer_count.as<unsigned int>() + 8;
+        p.u_count = st.mixed_ctr.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
         if (getenv("SG_BAND_DEBUG")) {  // development aid: how many pairs K0 diverted

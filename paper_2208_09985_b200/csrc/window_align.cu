@@ -1091,8 +1091,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 
     // Geometry of the next logical window of the current pair
     // (aligner.cpp:44-64). Returns 0 when the pair is complete (residues
-    // appended), 1 for a window, 2 (band pass) when the window is not a band
-    // window: the pair goes to the full-frame resume pass from here.
+    // appended), 1 for a window, 2 when the pair goes to another warp role (the
+    // queue in hand_to) before this window.
     auto next_window = [&]() -> int {
         const int n_rem = n_tot - toff, m_rem = m_tot - poff;
         if (n_rem == 0 || m_rem == 0) {
