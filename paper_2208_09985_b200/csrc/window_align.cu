@@ -1152,9 +1152,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     // Hand the pair to the next pass (the other frame) before its current window.
     auto defer_pair = [&]() {
         if (BAND && hand_to == 2 && nwin == 0 && P.u_list) {
-            // K0 (§3.10): the pair's first window already has D(0, 0) > 30: an
-            // unrelated pair (every window would go to a cooperative warp). The
-            // full-frame K1 after this kernel aligns it from the start.
+            // K0 (§3.10): the pair's first window already has D(0, 0) > 30 (an
+            // unrelated pair: every window would go to a cooperative warp) or is
+            // not band-shaped at all. The full-frame K1 after this kernel aligns
+            // it from the start.
             P.u_list[atomicAdd(P.u_count, 1u)] = pair;
             atomicSub(P.remaining, 1u);
             return;
