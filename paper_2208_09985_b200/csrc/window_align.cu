@@ -636,10 +636,13 @@ __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const Ban
         // another frame's parked row)
         if (live) reinterpret_cast<uint32_t*>(M.eqp + (c3 + 4) * 32)[1] = S.v[3];
         if (STORE_EV) {
+            // (old & keep) | acc as old * keep + acc on the FMA pipe: an event bit
+            // is set by at most one row of a window (X: D(i+1,j+1) <= d < D(i,j)
+            // and D(i,j) - D(i+1,j+1) <= 1; Y likewise), so old and acc are disjoint
             constexpr int SL3 = (U + 1) & 3;
             uint2 o;
-            o.x = (old.x & keep) | S.acc[SL3][0];
-            o.y = (old.y & keep) | S.acc[SL3][1];
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(o.x) : "r"(old.x), "r"(keep), "r"(S.acc[SL3][0]));
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(o.y) : "r"(old.y), "r"(keep), "r"(S.acc[SL3][1]));
             *px = o;
         }
     }
@@ -674,8 +677,9 @@ template <bool STD>
 __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K0, int k00,
                                           const BandMem& M, uint32_t two, uint32_t hmul) {
     const uint32_t lv = live ? ~0u : 0u;
-    // a live lane's first chunk of a window overwrites the events; otherwise OR
-    const uint32_t keep = live && d0 == 0 ? 0u : ~0u;
+    // a live lane's first chunk of a window overwrites the events; otherwise adds
+    // (as a multiplier: 0 or 1)
+    const uint32_t keep = live && d0 == 0 ? 0u : 1u;
     BandState S;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
