@@ -758,6 +758,16 @@ __device__ __forceinline__ int q_pop_n(uint32_t* q, int cap, int maxn, int* out)
     return take;
 }
 
+// Idle wait of at least `cycles` SM cycles (a single nanosleep can return after
+// a fraction of its argument; an idle warp's polls take issue slots and L2
+// bandwidth from the working warps).
+__device__ __forceinline__ void idle_wait(long long cycles) {
+    const long long t0 = clock64();
+    do {
+        __nanosleep(1000);
+    } while (clock64() - t0 < cycles);
+}
+
 // Warp-aggregated pop for the calling lanes that `want` a pair: one CAS on the
 // head claims up to one entry per such lane (a per-lane CAS serialises every pop
 // on one address).
@@ -1354,7 +1364,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             if (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
 
             // pairs are still in flight: one may be handed to this warp
-            __nanosleep(BAND ? 2000 : 8000);
+            idle_wait(BAND ? 4000 : 16000);
             ph_idle += clock64() - ck0;
             continue;
         }
@@ -1680,7 +1690,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
         pair = __shfl_sync(kFull, pair, 0);
         if (pair < 0) {
             if (*reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
-            __nanosleep(band::kCoopSleep);
+            idle_wait(2 * band::kCoopSleep);  // ~ns at 2 GHz
             continue;
         }
         // ---- restore the pair (every lane holds the same state; lane 0 writes)
