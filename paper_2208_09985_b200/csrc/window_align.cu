@@ -617,7 +617,6 @@ __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const Ban
     uint2 old = make_uint2(0u, 0u);
     if (STORE_EV) old = *px;
     const uint2 f = F[U];
-    if (MODE != kBDrain) F[U] = M.eqp[(col_top - U - 4 + 4) * 32];  // next group's column
     // rows 3..1 (descending: a row reads its upper row's value before it updates)
 #define SG_BCELL(r)                                                                   \
     if ((MODE == kBFill && (r) <= U) || (MODE == kBDrain && (r) > U) ||               \
@@ -628,8 +627,12 @@ __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const Ban
     if (MODE != kBDrain) {  // row 0: north = parked row of this column, masked for idle lanes
         S.eq[U] = f.x;
         band_cell<U, 0, CAP, STD>(S, f.y, two, hmul_l);
-        S.dg[0] = fma_shl(f.y, one_l);
+        // (right of the event columns the FMA pipe is the busier one: AND there)
+        S.dg[0] = MODE == kBOut ? f.y & (0u - one_l) : fma_shl(f.y, one_l);
         S.dgs[0] = STD ? fma_shr(f.y, hmul_l) : fma_shl(f.y, two_l);
+        // next group's column, into the registers f just left (no copies at the
+        // end of the group); used four steps on
+        F[U] = M.eqp[(col_top - U - 4 + 4) * 32];
     }
     if (ROW3) {
         // park row 3 (idle lanes do not: in a full-frame warp the slot may be
