@@ -410,8 +410,10 @@ __device__ __forceinline__ void sweep_group(Sweep<L, R>& S, Pref<L>& F, const La
                 _Pragma("unroll") for (int l = 0; l < L; ++l) pb[l] = S.v[R - 1][l];         \
             if (CAP) {                                                                       \
                 uint2 o;                                                                     \
-                o.x = F.ox | band_word<L>(S.acc[SL][0], mul); /* cleared per window */      \
-                o.y = F.oy | band_word<L>(S.acc[SL][1], mul);                                \
+                /* cleared per window; OR as an add on the FMA pipe: an event bit is set */ \
+                /* by one row at most */                                    \
+                o.x = dp_shift(F.ox, one, band_word<L>(S.acc[SL][0], mul));                  \
+                o.y = dp_shift(F.oy, one, band_word<L>(S.acc[SL][1], mul));                  \
                 *reinterpret_cast<uint2*>(px) = o;                                           \
                 if ((U) + 1 < R) { /* next step's column; groups reload at their start */   \
                     const uint2 n = *reinterpret_cast<const uint2*>(                         \
