@@ -353,3 +353,59 @@ def test_kernel_choice(gpu):
     assert kernel(2, 2000, 64, 24) == "full"
     assert kernel(5, 2000, 64, 24) == "full"
     assert kernel(4, 200, 256, 96) == "wide"
+
+
+def _stress_batch(sg, seed, n):
+    """Randomized long pairs: correlated reads at 0-25% edits of random mix,
+    unrelated pairs, garbage bursts (drifting windows), N bases."""
+    rng = np.random.default_rng(seed)
+    texts, pats = [], []
+    for _ in range(n):
+        L = int(np.exp(rng.uniform(np.log(60), np.log(4000))))
+        t = list(rng.integers(0, 4, L))
+        if rng.random() < 0.08:
+            p = list(rng.integers(0, 4, max(1, int(L * rng.uniform(0.5, 1.5)))))
+        else:
+            rate, mix = rng.uniform(0.0, 0.25), rng.dirichlet([1, 1, 1])
+            p = []
+            for ch in t[: int(L * rng.uniform(0.85, 1.0))]:
+                if rng.random() < rate:
+                    kind = rng.choice(3, p=mix)
+                    if kind == 0:
+                        p.append(int((ch + 1 + rng.integers(3)) % 4))
+                    elif kind == 1:
+                        p += [int(rng.integers(4)), ch]
+                else:
+                    p.append(ch)
+            if rng.random() < 0.05:
+                a = len(p) // 3
+                p = p[:a] + list(rng.integers(0, 4, int(rng.integers(30, 200)))) + p[a:]
+        if rng.random() < 0.02:
+            for _ in range(int(rng.integers(1, 6))):
+                t[int(rng.integers(len(t)))] = 4
+        texts.append(bytes(t))
+        pats.append(bytes(p if p else [0]))
+    return texts, pats
+
+
+@pytest.mark.parametrize("W,Ov,s,d,e", [(64, 24, 1, 1, 1), (64, 33, 0, 0, 0), (48, 16, 1, 0, 1)])
+def test_mixed_kernel_matches_full_frame(gpu, monkeypatch, W, Ov, s, d, e):
+    """K1 mixed (band + STD + cooperative warps, queues, K0 routing) against the
+    full-frame K1 on a randomized batch: every distance, CIGAR, window count and
+    counter identical; a sample is also checked against the oracle."""
+    sg = gpu
+    texts, pats = _stress_batch(sg, W * 7 + Ov, 4000)
+    codes = sg.CodesBatch.from_lists(texts, pats)
+    res = {}
+    for fr in ("band", "full"):
+        monkeypatch.setenv("SG_FRAME", fr)
+        res[fr] = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
+    a, b = res["band"], res["full"]
+    assert np.array_equal(np.asarray(a.distance), np.asarray(b.distance))
+    assert np.array_equal(np.asarray(a.windows), np.asarray(b.windows))
+    assert np.array_equal(np.asarray(a.counters), np.asarray(b.counters))
+    for k in range(len(texts)):
+        assert a.cigar_string(k) == b.cigar_string(k), k
+    for k in range(0, len(texts), 80):
+        o = O.align(texts[k], pats[k], W=W, O=Ov, sene=s, dent=d, et=e)
+        assert int(a.distance[k]) == o.distance and a.cigar_string(k) == o.cigar, k
