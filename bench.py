@@ -205,14 +205,24 @@ def reference_sample_size(threads: int) -> int:
     return int(min(100000, max(200, threads * 1200)))
 
 
+def kernel_source_sha():
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("window_align.cu", "window_align.cuh"):
+        with open(os.path.join(ROOT, "paper_2208_09985_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def traffic_bytes(pairs):
     """DRAM bytes (read + write) of one K1 launch, from the committed ncu --set full
-    capture of the same workload (profiles/k1_traffic.json); None if it does not
-    match this run's batch size."""
+    capture of the same workload (profiles/k1_traffic.json). None unless that capture
+    was taken of this kernel source (its sha) and this batch size: a stale figure is
+    not reported."""
     try:
         with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
             t = json.load(f)
-        if f"{pairs} pairs" not in t["workload"]:
+        if f"{pairs} pairs" not in t["workload"] or t.get("kernel_source_sha") != kernel_source_sha():
             return None
         return int(t["dram_bytes_read"]) + int(t["dram_bytes_write"])
     except (OSError, KeyError, ValueError):
@@ -263,125 +273,265 @@ def main_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------- per-config sweep
+
+# Every BASELINE.json config, each measured like the headline (SURVEY §8(d),
+# BASELINE.md §4): name, generator id, W, O, pairs, the CPU reference's rate per
+# core for sizing its bounded sample, description.
+CONFIGS = [
+    ("cfg1", 1, 64, 24, 10_000, 17000, "short plumbing: 110/100 bp, 5% edits 1:1:1"),
+    ("cfg2", 2, 64, 24, 1_000_000, 9600, "Illumina-like: 250 bp reads, 2% edits 8:1:1"),
+    ("cfg4_W32_O12", 4, 32, 12, 20_000, 240, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
+    ("cfg4_W64_O24", 4, 64, 24, 20_000, 182, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
+    ("cfg4_W64_O33", 4, 64, 33, 20_000, 166, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
+    ("cfg4_W128_O48", 4, 128, 48, 20_000, 110, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
+    ("cfg5", 5, 64, 24, 500_000, 300, "mixed 100..20k bp (log-uniform), 30% unrelated"),
+]
+
+
+def digest_parity(res, name):
+    """Every pair of a whole config against the reference's digests
+    (tests/golden/digests/<name>.tsv, make_digests.py): blocks bit-exact / total."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import golden_io as G
+        import oracle_ffi as Orc
+        blocks, pairs, total, _ = G.read_digests(name + ".tsv")
+        if pairs != res.n:
+            return None
+        got, tot = Orc.results_digests(res)
+        ok = sum(g == b[2] for g, b in zip(got, blocks))
+        return {"blocks_ok": ok, "blocks": len(blocks), "pairs": pairs,
+                "all_pairs_bit_exact": ok == len(blocks) and tot == total}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+
+
+def ref_sample(cfg_id, W_, O_, count, threads, switches=(1, 1, 1)):
+    tool = ref_tool_path()
+    if tool is None:
+        return None
+    s_, d_, e_ = switches
+    out = subprocess.run([tool, "bench", "--cfg", str(cfg_id), "--count", str(count),
+                          "--threads", str(threads), "--W", str(W_), "--O", str(O_),
+                          "--sene", str(s_), "--dent", str(d_), "--et", str(e_)],
+                         capture_output=True, text=True, check=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def measure_config(sg, name, cfg_id, W_, O_, pairs, rate_per_core, desc, steps, warmup, peak_ops,
+                   cpu, switches=(1, 1, 1)):
+    s_, d_, e_ = switches
+    cfg = sg.AlignerConfig(W=W_, O=O_, sene=bool(s_), dent=bool(d_), early_termination=bool(e_))
+    t_gen = time.perf_counter()
+    batch = sg.synth_packed(cfg_id, 0, pairs)
+    t_gen = time.perf_counter() - t_gen
+    sess = sg.Session(cfg, batch, 0)
+    for _ in range(warmup):
+        sess.run()
+    dev, k1 = [], []
+    for _ in range(steps):
+        ms, k = sess.run()
+        dev.append(ms)
+        k1.append(k)
+    info = sess.info()
+    res = sess.fetch()
+    sess.close()
+    cells = int(res.total.cells_computed)
+    alg_ops = 4 * ((W_ + 31) // 32) * cells
+    k1_s = sum(k1) / len(k1) / 1e3
+    parity = digest_parity(res, name)
+    launches = int(res.gpu_launches)
+    del res
+    sg.align_packed(cfg, batch)  # warm the one-shot path
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = sg.align_packed(cfg, batch)
+        del r
+    e2e_s = (time.perf_counter() - t0) / steps
+    h2d, d2h = sg.last_transfer_bytes()
+    out = {
+        "workload": f"{name}: {pairs:,} pairs, {desc}, W={W_} O={O_}, "
+                    f"sene={s_} dent={d_} et={e_}",
+        "value": round(pairs / (sum(dev) / len(dev) / 1e3), 1), "unit": UNIT,
+        "ms_per_step": round(sum(dev) / len(dev), 3),
+        "e2e": {"value": round(pairs / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "kernel": info["kernel"],
+        "roofline": {"bound": "int_alu", "achieved": round(alg_ops / k1_s / 1e12, 3),
+                     "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s (int32 lane-ops)",
+                     "frac": round(alg_ops / k1_s / peak_ops, 4), "alg_ops_per_launch": alg_ops,
+                     "k1_ms": round(1e3 * k1_s, 3)},
+        "gpu_launches_per_step": launches,
+        "parity": parity,
+        "gen_seconds": round(t_gen, 2),
+    }
+    if cpu:
+        threads = os.cpu_count() or 1
+        n = int(min(pairs, max(200, rate_per_core * threads * 3)))
+        try:
+            r = ref_sample(cfg_id, W_, O_, n, threads, switches)
+            if r is not None:
+                out["cpu_baseline"] = {
+                    "value": round(r["pairs_per_second"], 3), "unit": UNIT, "cores": threads,
+                    "kind": "reference",
+                    "sample": f"first {n:,} {name} pairs, {r['align_seconds']:.2f} s of run_batch"}
+                out["speedup_e2e_vs_cpu"] = round(out["e2e"]["value"] / r["pairs_per_second"], 1)
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"error": str(e)}
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 
 def main_ours(args):
     ws, rank, local = dist_env()
-    dist = Dist(ws, rank, local, args.backend)
     import paper_2208_09985_b200 as sg
     from paper_2208_09985_b200 import _ffi
     L = _ffi.load()
-    if L.sg_device_count() < 1:
+    visible = L.sg_device_count()
+    if visible < 1:
         raise SystemExit("bench.py: no CUDA device (the GPU path has no CPU fallback)")
-    device = local if ws > 1 else 0
+    # N GPUs: one rank per GPU under torchrun, else N devices driven from this process
+    inproc = ws == 1
+    n_gpus = ws if ws > 1 else args.gpus
+    if inproc and visible < n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but only {visible} CUDA device(s) visible")
+    devices = list(range(n_gpus)) if inproc else [local]
+    dist = Dist(ws, rank, local, args.backend)
     pairs = args.pairs
     cfg = sg.AlignerConfig(W=W, O=O, sene=True, dent=True, early_termination=True)
 
     from paper_2208_09985_b200 import shard
-    first, count = shard.rank_range(rank, ws, pairs)
     t_gen = time.perf_counter()
-    batch = sg.synth_packed(CFG_ID, first, count)
+    if inproc:  # device d aligns pairs [d*P, (d+1)*P) of the generator (weak scaling)
+        batches = [sg.synth_packed(CFG_ID, d * pairs, pairs) for d in devices]
+    else:
+        first, count = shard.rank_range(rank, ws, pairs)
+        batches = [sg.synth_packed(CFG_ID, first, count)]
     t_gen = time.perf_counter() - t_gen
-    sess = sg.Session(cfg, batch, device)
+    sessions = [sg.Session(cfg, b, d) for b, d in zip(batches, devices)]
 
-    # ---- device-resident: value
-    for _ in range(args.warmup):
-        sess.run()
-    info = sess.info()
-    sampler = ClockSampler(device)
+    # ---- device-resident: value. Each device's steps run on its own host thread;
+    # the job time is the max over devices (and ranks) of the summed CUDA-event times.
+    def run_steps(k, n_steps, out=None, barrier=None):
+        if barrier is not None:
+            barrier.wait()
+        for _ in range(n_steps):
+            ms, k1 = sessions[k].run()
+            if out is not None:
+                out[k].append((ms, k1))
+
+    def on_all(n_steps, out=None):
+        if len(sessions) == 1:
+            run_steps(0, n_steps, out)
+            return
+        bar = threading.Barrier(len(sessions))
+        th = [threading.Thread(target=run_steps, args=(k, n_steps, out, bar))
+              for k in range(len(sessions))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    on_all(args.warmup)
+    info = sessions[0].info()
+    sampler = ClockSampler(devices[0])
     sampler.start()
     dist.barrier()
     cuda_sync()
-    dev_ms, k1_ms = [], []
+    times = [[] for _ in sessions]
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        ms, k1 = sess.run()
-        dev_ms.append(ms)
-        k1_ms.append(k1)
+    on_all(args.steps, times)
     cuda_sync()
     dist.barrier()
     wall = time.perf_counter() - t0
     clocks = sampler.stop()
-    total_ms = dist.max(sum(dev_ms))
-    value = ws * pairs * args.steps / (total_ms / 1e3)
+    total_ms = dist.max(max(sum(ms for ms, _ in t) for t in times))
+    value = n_gpus * pairs * args.steps / (total_ms / 1e3)
+    k1_ms = [k1 for ms, k1 in times[0]]
 
-    res = sess.fetch()
-    launches_per_step = int(res.gpu_launches)
+    res = sessions[0].fetch()
+    launches_per_step = int(res.gpu_launches) * len(sessions)
     cells = int(res.total.cells_computed)
     alg_ops = 4 * ((W + 31) // 32) * cells
     k1_avg_s = sum(k1_ms) / len(k1_ms) / 1e3
     achieved = alg_ops / k1_avg_s
 
-    # parity sample against the reference's golden vectors (rank 0 holds pairs 0..)
+    # parity: every pair of device 0's batch (rank 0 at N=1 holds cfg3's 100k pairs)
+    # against the reference's whole-config digests
     parity = None
-    if rank == 0:
-        try:
-            sys.path.insert(0, os.path.join(ROOT, "tests"))
-            import golden_io as G
-            import oracle_ffi as Orc
-            ok = tot = 0
-            for name in ("cfg3_head.tsv", "cfg3_tail.tsv"):
-                for row in G.read_golden(name):
-                    k = G.pair_index(row["id"])
-                    if k >= pairs:
-                        continue
-                    cig = res.cigar_string(k)
-                    tot += 1
-                    ok += (int(res.distance[k]) == row["distance"] and
-                           Orc.fnv1a(cig) == row["hash"] and int(res.windows[k]) == row["windows"]
-                           and [int(x) for x in res.counters[k]] == row["counters"])
-            parity = f"{ok}/{tot} pairs bit-exact vs reference golden vectors"
-        except Exception as e:  # pragma: no cover
-            parity = f"unchecked ({e})"
-    sess.close()
+    if rank == 0 and pairs == 100000 and (inproc or ws == 1):
+        parity = digest_parity(res, "cfg3")
+    for s_ in sessions:
+        s_.close()
     del res
 
     # ---- measured ALU peak (roofline denominator)
     import ctypes as C
     r_alu, mhz_peak, ops_s = C.c_double(), C.c_double(), C.c_double()
-    L.sg_alu_peak(device, C.byref(r_alu), C.byref(mhz_peak), C.byref(ops_s))
+    L.sg_alu_peak(devices[0], C.byref(r_alu), C.byref(mhz_peak), C.byref(ops_s))
     sm_mhz = clocks["sm_mhz"] if clocks else mhz_peak.value
     peak = info["sms"] * r_alu.value * sm_mhz * 1e6
 
-    # ---- end to end through the C ABI with host buffers: e2e
+    # ---- end to end through the C ABI with host buffers: e2e. In one process the
+    # library splits one batch of N x P pairs over the N devices itself (K5).
+    if inproc and n_gpus > 1:
+        e2e_batch = sg.synth_packed(CFG_ID, 0, n_gpus * pairs)
+    else:
+        e2e_batch = batches[0]
+    e2e_devices = devices
     for _ in range(max(1, args.warmup // 2)):
-        sg.align_packed(cfg, batch, devices=[device])
+        sg.align_packed(cfg, e2e_batch, devices=e2e_devices)
     dist.barrier()
     cuda_sync()
     t0 = time.perf_counter()
     h2d = d2h = 0
     for _ in range(args.steps):
-        r = sg.align_packed(cfg, batch, devices=[device])
+        r = sg.align_packed(cfg, e2e_batch, devices=e2e_devices)
         h2d, d2h = sg.last_transfer_bytes()
         del r
     cuda_sync()
     dist.barrier()
     e2e_s = dist.max(time.perf_counter() - t0)
-    e2e = ws * pairs * args.steps / e2e_s
+    e2e = n_gpus * pairs * args.steps / e2e_s
 
     base = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         try:
             base = cpu_baseline(os.cpu_count() or 1)
         except Exception as e:  # pragma: no cover
             base = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                     "sample": f"failed: {e}"}
 
+    # ---- every other BASELINE config (N = 1, rank 0): BASELINE.md §4's table
+    per_config = None
+    if rank == 0 and n_gpus == 1 and not args.headline_only:
+        del batches, e2e_batch
+        per_config = {}
+        for (name, cid, w_, o_, n_, rate, desc) in CONFIGS:
+            per_config[name] = measure_config(sg, name, cid, w_, o_, n_, rate, desc,
+                                              args.config_steps, args.warmup, peak,
+                                              not args.no_cpu_baseline)
+
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32 bitvectors (int)",
             "data": "synthetic (seeded cfg3 generator)",
             "config": {"workload": WORKLOAD, "pairs_per_gpu": pairs, "W": W, "O": O,
-                       "parallelism": f"pairs sharded over {ws} GPU(s), no collective",
+                       "parallelism": (f"{n_gpus} GPU(s) driven from one process, "
+                                       "pairs sharded, no collective") if inproc else
+                                      f"one rank per GPU ({ws}), pairs sharded, no collective",
                        "l2": "inputs 0.5 GB/GPU > 126 MB L2, no flush needed",
-                       "resident_lanes": info["lanes"]},
+                       "resident_lanes": info["lanes"], "kernel": info["kernel"]},
             "roofline": {"bound": "int_alu", "achieved": round(achieved / 1e12, 3),
                          "peak": round(peak / 1e12, 3), "unit": "Tops/s (int32 lane-ops)",
                          "frac": round(achieved / peak, 4), "traffic": traffic_bytes(pairs),
-                         "traffic_unit": "DRAM bytes per K1 launch (ncu, profiles/k1_traffic.json)",
+                         "traffic_unit": "DRAM bytes per K1 launch (ncu --set full of this "
+                                         "kernel build, profiles/k1_traffic.json)",
                          "alg_ops_per_launch": alg_ops, "cells_computed": cells,
                          "k1_ms": round(sum(k1_ms) / len(k1_ms), 3),
                          "r_alu_ops_per_clk_per_sm": round(r_alu.value, 2),
@@ -393,6 +543,7 @@ def main_ours(args):
             "clocks": clocks,
             "parity": parity,
             "cpu_baseline": base,
+            "configs": per_config,
             "host": {"gen_seconds": round(t_gen, 2), "wall_s_timed": round(wall, 3)},
         }
         print(json.dumps(line), flush=True)
@@ -409,6 +560,9 @@ def main():
     ap.add_argument("--pairs", type=int, default=100000, help="pairs per GPU (cfg3: 100000)")
     ap.add_argument("--backend", default="nccl", help="torch.distributed backend for N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the per-config sweep (cfg1, cfg2, cfg4 x 4, cfg5) at N = 1")
+    ap.add_argument("--config-steps", type=int, default=3, help="timed steps per config")
     args = ap.parse_args()
     if args.impl == "reference":
         return main_reference(args)

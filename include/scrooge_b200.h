@@ -52,7 +52,8 @@ enum {
 
 /* AlignerConfig, proj/include/scrooge/aligner.hpp:12-31. Defaults W=64, O=33,
  * all switches on (sg_config_default). single_window selects
- * Mode::SingleWindow (not supported on the GPU path yet: SG_CONFIG). */
+ * Mode::SingleWindow (align_single_window, aligner.cpp:87-112) with edit budget
+ * k_single; sequences of up to 1024 characters (K1 up to 128, K6 above). */
 typedef struct sg_config {
     int32_t W;
     int32_t O;
@@ -159,9 +160,44 @@ int64_t sg_cigar_runs(const sg_results* res, int64_t k, char* ops, int64_t* lens
 int sg_pack(const sg_pairs* in, sg_packed_pairs* out);
 void sg_packed_free(sg_packed_pairs* p);
 
+/* K5, the device split of a batch, on the host alone: pair k goes
+ * to device slot shard[k] (0 .. n_devices-1) at position pos[k] of that device's
+ * batch. *gathered = 0 when the shards are contiguous ranges of input order
+ * (pairs of near-equal estimated cost), 1 when the pairs were sorted into cost
+ * buckets and dealt longest-first to the least-loaded device (cfg5's mix).
+ * sg_align_batch / sg_align_packed use exactly this split for n_devices > 1. */
+int sg_plan_shards(const sg_packed_pairs* pairs, int n_devices, int32_t* shard, int64_t* pos,
+                   int* gathered);
+
 /* Bytes copied host->device (direction 0) / device->host (1) by the last
  * sg_align_batch / sg_align_packed call on this thread. */
 int64_t sg_last_transfer_bytes(int direction);
+
+/* Process-wide execution options. They select among equivalent device paths for
+ * cross-checks, A/B measurements and diagnostics; no option changes a result.
+ * Defaults (sg_options_default) are what the library picks on its own. Set them
+ * between calls, not while a call is running. */
+enum {
+    SG_KERNEL_AUTO = 0,   /* the host's choice per shard */
+    SG_KERNEL_FULL = 1,   /* full-frame K1 (one pair per lane) */
+    SG_KERNEL_MIXED = 2,  /* mixed band / cooperative K1 where the window shape allows */
+    SG_KERNEL_WIDE = 3    /* K6 (one pair per warp) for every batch */
+};
+enum {
+    SG_DIAG_WARP_TIMES = 1,   /* per-warp start/exit timeline of sessions' K1 */
+    SG_DIAG_PHASE_CYCLES = 2, /* per-phase SM cycles of sessions' K1 */
+    SG_DIAG_HOST_TRACE = 4    /* host pipeline timestamps on stderr */
+};
+typedef struct sg_options {
+    int32_t kernel;         /* SG_KERNEL_* */
+    int32_t stream_upload;  /* 1: one-shot calls overlap the sequence H2D with K1 */
+    int32_t longest_first;  /* 1: pairs of different lengths start longest first */
+    int32_t diagnostics;    /* SG_DIAG_* bits */
+    int64_t exact_budget;   /* K7 delta-store bytes per batch; 0 = half the free memory */
+} sg_options;
+void sg_options_default(sg_options* o);
+int sg_set_options(const sg_options* o); /* SG_CONFIG for an unknown kernel */
+void sg_get_options(sg_options* o);
 
 /* Device-resident sessions (inputs already in HBM when timing starts). */
 typedef struct sg_session sg_session;
@@ -177,6 +213,12 @@ int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* 
  * counterpart. */
 int sg_session_kernel(const sg_session* s);
 void sg_session_destroy(sg_session* s);
+/* Diagnostics of the session's last run with SG_DIAG_PHASE_CYCLES / SG_DIAG_WARP_TIMES
+ * set: 25 per-phase counters (setup, DC, TB, ... cycles summed over warps), or
+ * per-warp (start, exit, smid) triples (returns the warp count, <= cap). -1 when
+ * the run did not collect them. */
+int sg_session_phase_cycles(sg_session* s, uint64_t* out25);
+int sg_session_warp_times(sg_session* s, uint64_t* out, int cap);
 
 /* Measured integer-ALU issue rate of `device` (LOP3 lane-ops per clock per SM,
  * the clock the microbenchmark ran at, and lane-ops/s) — the roofline

@@ -637,3 +637,106 @@ int64_t orc_worst_quantile(int64_t* scores, int64_t n, double p) {
     if (rank > n) rank = n;
     return scores[rank - 1];
 }
+
+/* ---- whole-config digests (tests/golden/make_digests.py, ref_tool.cpp:digest_line) ---- */
+
+#define FNV_OFF 1469598103934665603ull
+#define FNV_PRIME 1099511628211ull
+
+static uint64_t fnv_bytes(uint64_t h, const char* s, size_t len) {
+    for (size_t k = 0; k < len; ++k) h = (h ^ (unsigned char)s[k]) * FNV_PRIME;
+    return h;
+}
+
+typedef struct digest_job {
+    int64_t b_lo, b_hi, n_pairs, block;
+    const int64_t* distance;
+    const int32_t* windows;
+    const uint8_t* found;
+    const int64_t* cigar_off;
+    const uint8_t* runs;
+    const uint64_t* counters;
+    uint64_t* digests;
+} digest_job;
+
+/* fnv1a64 of cigar_to_string (cigar.cpp:18-25) of one pair's run bytes and its run count. */
+static uint64_t cigar_hash(const uint8_t* r, int64_t nbytes, int64_t* n_runs) {
+    static const char opc[4] = {'=', 'X', 'I', 'D'};
+    uint64_t h = FNV_OFF;
+    int64_t runs = 0;
+    char num[32];
+    for (int64_t k = 0; k < nbytes;) {
+        const int op = r[k] >> 6;
+        int64_t len = 0;
+        while (k < nbytes && (r[k] >> 6) == op) len += (r[k++] & 63) + 1;
+        const int w = snprintf(num, sizeof num, "%lld%c", (long long)len, opc[op]);
+        h = fnv_bytes(h, num, (size_t)w);
+        ++runs;
+    }
+    *n_runs = runs;
+    return h;
+}
+
+static void* digest_worker(void* arg) {
+    digest_job* j = (digest_job*)arg;
+    char line[512];
+    for (int64_t b = j->b_lo; b < j->b_hi; ++b) {
+        const int64_t lo = b * j->block;
+        const int64_t hi = lo + j->block < j->n_pairs ? lo + j->block : j->n_pairs;
+        uint64_t h = FNV_OFF;
+        for (int64_t k = lo; k < hi; ++k) {
+            int64_t n_runs = 0;
+            uint64_t ch;
+            if (j->found && !j->found[k]) {
+                ch = fnv_bytes(FNV_OFF, "*", 1);
+            } else {
+                ch = cigar_hash(j->runs + j->cigar_off[k], j->cigar_off[k + 1] - j->cigar_off[k],
+                                &n_runs);
+            }
+            const uint64_t* c = j->counters + 7 * k;
+            const int w = snprintf(line, sizeof line,
+                                   "%lld\t%016llx\t%lld\t%d\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\n",
+                                   (long long)j->distance[k], (unsigned long long)ch,
+                                   (long long)n_runs, (int)j->windows[k], (unsigned long long)c[0],
+                                   (unsigned long long)c[1], (unsigned long long)c[2],
+                                   (unsigned long long)c[3], (unsigned long long)c[4],
+                                   (unsigned long long)c[5], (unsigned long long)c[6]);
+            h = fnv_bytes(h, line, (size_t)w);
+        }
+        j->digests[b] = h;
+    }
+    return NULL;
+}
+
+uint64_t orc_digest_blocks(int64_t n_pairs, const int64_t* distance, const int32_t* windows,
+                           const uint8_t* found, const int64_t* cigar_off, const uint8_t* runs,
+                           const uint64_t* counters, int64_t block, uint64_t* digests,
+                           int threads) {
+    if (block < 1) block = 1;
+    if (threads < 1) threads = 1;
+    if (threads > 128) threads = 128;
+    const int64_t n_blocks = (n_pairs + block - 1) / block;
+    pthread_t th[128];
+    digest_job jobs[128];
+    const int64_t per = (n_blocks + threads - 1) / threads;
+    int started = 0;
+    for (int t = 0; t < threads; ++t) {
+        digest_job* j = &jobs[t];
+        j->b_lo = t * per;
+        j->b_hi = j->b_lo + per < n_blocks ? j->b_lo + per : n_blocks;
+        if (j->b_lo >= j->b_hi) break;
+        j->n_pairs = n_pairs; j->block = block; j->distance = distance; j->windows = windows;
+        j->found = found; j->cigar_off = cigar_off; j->runs = runs; j->counters = counters;
+        j->digests = digests;
+        pthread_create(&th[t], NULL, digest_worker, j);
+        ++started;
+    }
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    uint64_t total = FNV_OFF;
+    char hex[32];
+    for (int64_t b = 0; b < n_blocks; ++b) {
+        snprintf(hex, sizeof hex, "%016llx", (unsigned long long)digests[b]);
+        total = fnv_bytes(total, hex, 16);
+    }
+    return total;
+}

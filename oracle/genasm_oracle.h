@@ -87,6 +87,17 @@ int64_t orc_score_cigar(const orc_result* r, int match_bonus, int mismatch_penal
 /* worst_quantile (proj/src/sweep.cpp:11-19); scores are sorted in place. */
 int64_t orc_worst_quantile(int64_t* scores, int64_t n, double p);
 
+/* Per-block digests of a batch's results, as `ref_tool digest` computes them from
+ * the reference's BatchResult (oracle/ref_tool.cpp:digest_line): per pair the line
+ * "distance\tfnv(cigar_to_string)\truns\twindows\t<7 counters>\n" (the CIGAR of a
+ * not-found pair is "*"), and per block of `block` pairs fnv1a64 over its lines.
+ * Inputs are the GPU path's sg_results arrays (run bytes as orc_replay_runs).
+ * Writes ceil(n/block) digests; returns fnv1a64 over their 16-hex-digit forms. */
+uint64_t orc_digest_blocks(int64_t n_pairs, const int64_t* distance, const int32_t* windows,
+                           const uint8_t* found, const int64_t* cigar_off, const uint8_t* runs,
+                           const uint64_t* counters, int64_t block, uint64_t* digests,
+                           int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,8 @@
 //   ref_tool align  --input pairs.tsv [cfg flags] [--hash]   per-pair results
 //   ref_tool synth  --cfg N --first F --count C [cfg flags] [--hash]
 //   ref_tool bench  --cfg N --first F --count C --threads T [cfg flags]
+//   ref_tool digest --cfg N [--first F --count C] [--block B] [cfg flags]
+//                   per-block FNV-1a digests of every pair's result (see digest_line)
 //   ref_tool read --input pairs.tsv | read-fasta --input a.fa,b.fa   parsed pairs
 //   ref_tool cli-tsv --input pairs.tsv [cfg flags]   write_batch_tsv output
 //   ref_tool simulate --count C --length L --rate R --seed S   simulate_pairs TSV
@@ -43,6 +45,7 @@ struct Args {
     int cfg = 1;
     long long first = 0, count = -1;
     int threads = 1;
+    long long block = 1000;
     bool hash = false;
     int length = 0;
     double rate = 0;
@@ -73,6 +76,7 @@ Args parse(int argc, char** argv) {
         else if (k == "--count") a.count = std::stoll(val());
         else if (k == "--threads") a.threads = std::stoi(val());
         else if (k == "--hash") a.hash = true;
+        else if (k == "--block") a.block = std::stoll(val());
         else if (k == "--length") a.length = std::stoi(val());
         else if (k == "--rate") a.rate = std::stod(val());
         else if (k == "--seed") a.seed = std::stoull(val());
@@ -136,6 +140,56 @@ void print_results(const std::vector<scrooge::SeqPairRecord>& pairs, const scroo
                     (unsigned long long)c.cells_computed, (unsigned long long)c.rows_possible,
                     (unsigned long long)c.baseline_equiv_bits);
     }
+}
+
+// One pair's record in the digest: distance, fnv1a64(cigar_to_string) as 16 hex
+// digits, run count, windows, the 7 counters, tab-separated, '\n'-terminated
+// ("*" hashes for not-found pairs, as print_results). A block's digest is fnv1a64
+// over its pairs' records in input order; the total is fnv1a64 over the block
+// digests' 16-hex-digit forms. tests/golden/digest.py and oracle/genasm_oracle.c
+// (orc_digest_block) compute the same from the GPU's results.
+std::string digest_line(const scrooge::PairOutcome& po) {
+    const std::string cig = po.found ? scrooge::cigar_to_string(po.cigar) : "*";
+    const auto& c = po.counters;
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%lld\t%016llx\t%zu\t%d\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\t%llu\n",
+                  static_cast<long long>(po.distance), static_cast<unsigned long long>(fnv1a(cig)),
+                  po.cigar.size(), po.windows, (unsigned long long)c.stored_bits,
+                  (unsigned long long)c.table_writes, (unsigned long long)c.table_reads,
+                  (unsigned long long)c.rows_computed, (unsigned long long)c.cells_computed,
+                  (unsigned long long)c.rows_possible, (unsigned long long)c.baseline_equiv_bits);
+    return buf;
+}
+
+void run_digest(Args a) {
+    sg_synth_spec spec;
+    if (!sg_synth_baseline_spec(a.cfg, &spec)) throw scrooge::InputError("bad --cfg");
+    const long long first = a.first, count = a.count < 0 ? spec.n_pairs - a.first : a.count;
+    const long long chunk = std::max<long long>(a.block, (20000 / a.block) * a.block);
+    std::uint64_t total = 1469598103934665603ull;
+    std::uint64_t cells = 0;
+    for (long long c0 = 0; c0 < count; c0 += chunk) {
+        Args sub = a;
+        sub.first = first + c0;
+        sub.count = std::min(chunk, count - c0);
+        const auto pairs = synth_pairs(sub);
+        const scrooge::BatchResult br = scrooge::run_batch(pairs, a.config, a.threads);
+        for (long long b0 = 0; b0 < sub.count; b0 += a.block) {
+            const long long bn = std::min(a.block, sub.count - b0);
+            std::string recs;
+            for (long long q = b0; q < b0 + bn; ++q) {
+                recs += digest_line(br.outcomes[static_cast<std::size_t>(q)]);
+                cells += br.outcomes[static_cast<std::size_t>(q)].counters.cells_computed;
+            }
+            char hex[32];
+            std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a(recs)));
+            for (const char* h = hex; *h; ++h) total = (total ^ static_cast<unsigned char>(*h)) * 1099511628211ull;
+            std::printf("%lld\t%lld\t%s\n", sub.first + b0, bn, hex);
+        }
+        std::fflush(stdout);
+    }
+    std::printf("total\t%lld\t%016llx\t%llu\n", count, static_cast<unsigned long long>(total),
+                static_cast<unsigned long long>(cells));
 }
 
 }  // namespace
@@ -214,6 +268,8 @@ int main(int argc, char** argv) {
         } else if (a.cmd == "synth") {
             const auto pairs = synth_pairs(a);
             print_results(pairs, scrooge::run_batch(pairs, a.config, a.threads), a.hash);
+        } else if (a.cmd == "digest") {
+            run_digest(a);
         } else if (a.cmd == "bench") {
             const auto pairs = synth_pairs(a);
             const scrooge::BatchResult br = scrooge::run_batch(pairs, a.config, a.threads);

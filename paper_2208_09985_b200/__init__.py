@@ -11,6 +11,6 @@ from .aligner import (  # noqa: F401
     cigar_from_string, cigar_to_string, decode_sequence, encode_sequence, last_transfer_bytes,
     pack, run_batch, synth_codes, synth_packed, write_batch_tsv, PairFile, read_pairs,
     write_results, ScoringParams, score_cigar, worst_quantile, global_align,
-    global_align_packed, GlobalAlignment, SweepRow, run_sweep, sweep_csv, sweep_json,
+    global_align_packed, GlobalAlignment, SweepRow, run_sweep, sweep_csv, sweep_json, options,
 )
 from .build import LIB as LIBRARY_PATH  # noqa: F401

@@ -25,8 +25,12 @@ EXPORTS = (
     "sg_session_info", "sg_session_kernel", "sg_session_destroy", "sg_synth_packed", "sg_synth_codes",
     "sg_pairs_free", "sg_alu_peak", "sg_read_pairs", "sg_pair_file_free", "sg_write_results",
     "sg_global_align", "sg_scoring_default", "sg_score_cigar", "sg_worst_quantile", "sg_sweep",
-    "sg_sweep_format",
+    "sg_sweep_format", "sg_options_default", "sg_set_options", "sg_get_options",
+    "sg_session_phase_cycles", "sg_session_warp_times", "sg_plan_shards",
 )
+
+SG_KERNEL = {"auto": 0, "full": 1, "mixed": 2, "wide": 3}
+SG_DIAG_WARP_TIMES, SG_DIAG_PHASE_CYCLES, SG_DIAG_HOST_TRACE = 1, 2, 4
 
 
 class SgConfig(C.Structure):
@@ -71,6 +75,11 @@ class SgSweepRow(C.Structure):
                 ("pairs_per_s", C.c_double), ("oracle_q500", C.c_int64),
                 ("oracle_q100", C.c_int64), ("oracle_q010", C.c_int64),
                 ("oracle_q001", C.c_int64)]
+
+
+class SgOptions(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("stream_upload", C.c_int32), ("longest_first", C.c_int32),
+                ("diagnostics", C.c_int32), ("exact_budget", C.c_int64)]
 
 
 class SgResults(C.Structure):
@@ -146,6 +155,14 @@ def load(build_if_missing: bool = True):
     L.sg_sweep.argtypes = [P(SgSweepOptions), P(SgPackedPairs), P(C.c_int), C.c_int, P(SgSweepRow)]
     L.sg_sweep_format.argtypes = [P(SgSweepRow), C.c_int64, C.c_int, C.c_char_p, C.c_int64]
     L.sg_sweep_format.restype = C.c_int64
+    L.sg_options_default.argtypes = [P(SgOptions)]
+    L.sg_options_default.restype = None
+    L.sg_set_options.argtypes = [P(SgOptions)]
+    L.sg_get_options.argtypes = [P(SgOptions)]
+    L.sg_get_options.restype = None
+    L.sg_session_phase_cycles.argtypes = [C.c_void_p, P(C.c_uint64)]
+    L.sg_session_warp_times.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int]
+    L.sg_plan_shards.argtypes = [P(SgPackedPairs), C.c_int, C.c_void_p, C.c_void_p, P(C.c_int)]
     _lib = L
     return L
 

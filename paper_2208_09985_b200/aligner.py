@@ -25,6 +25,7 @@ is no CPU fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import re
 from dataclasses import dataclass, field
@@ -459,6 +460,36 @@ def last_transfer_bytes():
     return int(L.sg_last_transfer_bytes(0)), int(L.sg_last_transfer_bytes(1))
 
 
+@contextlib.contextmanager
+def options(kernel: Optional[str] = None, stream_upload: Optional[bool] = None,
+            longest_first: Optional[bool] = None, diagnostics: Optional[int] = None,
+            exact_budget: Optional[int] = None):
+    """Process-wide execution options (sg_set_options) for the duration of a block:
+    which K1 runs ("auto", "full", "mixed", "wide"), the streamed upload, the
+    longest-first order, diagnostics bits and K7's memory budget. They pick among
+    equivalent device paths for cross-checks and measurements; none changes a result."""
+    L = _ffi.load()
+    old = _ffi.SgOptions()
+    L.sg_get_options(C.byref(old))
+    new = _ffi.SgOptions()
+    C.memmove(C.byref(new), C.byref(old), C.sizeof(old))
+    if kernel is not None:
+        new.kernel = _ffi.SG_KERNEL[kernel]
+    if stream_upload is not None:
+        new.stream_upload = int(bool(stream_upload))
+    if longest_first is not None:
+        new.longest_first = int(bool(longest_first))
+    if diagnostics is not None:
+        new.diagnostics = int(diagnostics)
+    if exact_budget is not None:
+        new.exact_budget = int(exact_budget)
+    _check(L.sg_set_options(C.byref(new)))
+    try:
+        yield
+    finally:
+        L.sg_set_options(C.byref(old))
+
+
 class Session:
     """Device-resident batch on one GPU: inputs uploaded once, kernels re-run."""
 
@@ -484,6 +515,21 @@ class Session:
         _ffi.load().sg_session_info(self._h, C.byref(lanes), C.byref(sms), C.byref(limbs))
         kernel = ("full", "mixed", "wide")[_ffi.load().sg_session_kernel(self._h)]
         return {"lanes": lanes.value, "sms": sms.value, "limbs": limbs.value, "kernel": kernel}
+
+    def phase_cycles(self):
+        """Per-phase cycle counters of the last run under options(diagnostics=2)."""
+        buf = (C.c_uint64 * 25)()
+        if _ffi.load().sg_session_phase_cycles(self._h, buf) != 0:
+            return None
+        return list(buf)
+
+    def warp_times(self, cap: int = 8192):
+        """(start, exit, smid) per warp of the last run under options(diagnostics=1)."""
+        buf = (C.c_uint64 * (3 * cap))()
+        n = _ffi.load().sg_session_warp_times(self._h, buf, cap)
+        if n < 0:
+            return None
+        return [tuple(buf[3 * k:3 * k + 3]) for k in range(n)]
 
     def close(self):
         if self._h:

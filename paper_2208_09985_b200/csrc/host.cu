@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -84,6 +86,34 @@ void parallel_for(int64_t n, F&& f, int64_t grain = 1024) {
     }
     for (auto& th : pool) th.join();
 }
+
+// ------------------------------------------------------------ options, device guard
+
+std::mutex g_opt_mu;
+sg_options g_opt = {SG_KERNEL_AUTO, 1, 1, 0, 0};
+
+sg_options options() {
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    return g_opt;
+}
+
+// Restores the caller's current device when an ABI call returns: the library
+// must not change the host application's CUDA device (a drop-in sits next to
+// PyTorch and others that rely on it).
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // ------------------------------------------------------------ pinned host memory
 
@@ -193,6 +223,7 @@ struct DevState {
     DevBuf bnd_ones, bnd_zeros;      // constant parked rows (one warp's slots, L = 4 size)
     cudaStream_t copy = nullptr;     // H2D of the sequence words, overlapping K1
     cudaEvent_t copy_go = nullptr;
+    cudaEvent_t copy_done = nullptr; // the last piece of the upload (joined before K2)
     int64_t chunk_words = 1;
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
@@ -200,6 +231,9 @@ struct DevState {
     // the handed pairs' state, K0's list of unrelated pairs
     DevBuf q_band, q_full, q_coop, q_std, mixed_ctr, resume_state, u_list;
     long long grid = 0, lanes = 0;
+    // diagnostics (SG_DIAG_*) of the last launch on this device
+    DevBuf diag_warp, diag_phase;
+    int diag_warps = 0, diag_flags = 0;
 
     void init(int dev) {
         device = dev;
@@ -208,6 +242,7 @@ struct DevState {
         SG_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         SG_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
         SG_CUDA_CHECK(cudaEventCreateWithFlags(&copy_go, cudaEventDisableTiming));
+        SG_CUDA_CHECK(cudaEventCreateWithFlags(&copy_done, cudaEventDisableTiming));
         for (auto& e : ev) SG_CUDA_CHECK(cudaEventCreate(&e));
     }
     ~DevState() {
@@ -218,10 +253,11 @@ struct DevState {
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
                           &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state,
-                          &u_list})
+                          &u_list, &diag_warp, &diag_phase})
             b->release();
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
+        if (copy_done) cudaEventDestroy(copy_done);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         cudaStreamDestroy(stream);
@@ -439,9 +475,9 @@ uint32_t bases8(const uint32_t* seq, int64_t a) {  // 8 bases (16 bits) from bas
     return static_cast<uint32_t>(w >> (2 * (a & 15))) & 0xFFFFu;
 }
 
-bool pair_related(const sg_packed_pairs* in, int64_t k) {
+bool pair_related(const sg_packed_pairs* in, int64_t k, int64_t span = 256, int need = 2) {
     const int64_t n = in->text_len[k], m = in->pat_len[k];
-    const int64_t len = std::min<int64_t>(std::min(n, m), 256);
+    const int64_t len = std::min<int64_t>(std::min(n, m), span);
     if (len < 128) return true;
     const int64_t ta = in->text_off[k], pa = in->pat_off[k];
     int hits = 0;
@@ -450,14 +486,16 @@ bool pair_related(const sg_packed_pairs* in, int64_t k) {
         for (int64_t dl = -16; dl <= 16; ++dl) {
             const int64_t j = b + dl;
             if (j < 0 || j + 8 > m) continue;
-            if (bases8(in->seq, pa + j) == t && ++hits >= 2) return true;
+            if (bases8(in->seq, pa + j) == t && ++hits >= need) return true;
         }
     }
     return false;
 }
 
 bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) {
-    if (const char* e = getenv("SG_FRAME")) return e[0] == 'b';  // experiments: band / full
+    const int kernel = options().kernel;
+    if (kernel == SG_KERNEL_MIXED) return true;
+    if (kernel == SG_KERNEL_FULL) return false;
     const int64_t n = hi - lo;
     if (n <= 0) return false;
     double tot = 0;
@@ -544,7 +582,7 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split
     }
     pp.any_n = any_n;
     pp.scratch_bytes = bound;
-    pp.ordered = longest_first && n > 1 && !getenv("SG_NO_LPT");  // env: experiments
+    pp.ordered = longest_first && n > 1 && options().longest_first;
     if (pp.ordered) {
         pp.order.ensure(4 * static_cast<size_t>(n));
         int32_t* o = pp.order.as<int32_t>();
@@ -587,10 +625,6 @@ struct RunConfig {
     int wcap;   // K6: widest window in columns
 };
 
-unsigned long long* g_phase_buf = nullptr;  // diagnostics (SG_PHASE_CYCLES=1)
-unsigned long long* g_warp_times = nullptr;  // diagnostics (SG_WARP_TIMES=1)
-int g_warp_count = 0;
-
 // Single-window mode sizes the vectors by the longest sequence of the batch.
 RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = nullptr,
                      const int64_t* pl = nullptr) {
@@ -605,16 +639,15 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
         r.L = limbs_for(static_cast<int>(mx));
         r.wcap = static_cast<int>(mx);
     }
-    // K6 takes what K1's limb counts do not cover; SG_FORCE_WIDE=1 routes every
+    // K6 takes what K1's limb counts do not cover; SG_KERNEL_WIDE routes every
     // batch through it (tests cross-check the two kernels)
-    const char* fw = getenv("SG_FORCE_WIDE");
-    r.wide = r.L == 0 || (fw && fw[0] == '1');
+    const int kernel = options().kernel;
+    r.wide = r.L == 0 || kernel == SG_KERNEL_WIDE;
     r.W = c->W;
     r.O = c->O;
     r.et = c->early_termination ? 1 : 0;
     r.policy = c->dent ? 2 : c->sene ? 1 : 0;
-    const char* nb = getenv("SG_NO_BAND");  // experiments / cross-checks: full frame only
-    r.band = !r.wide && sgk::band_eligible(r.W, r.O, r.single) && !(nb && nb[0] == '1');
+    r.band = !r.wide && sgk::band_eligible(r.W, r.O, r.single) && kernel != SG_KERNEL_FULL;
     return r;
 }
 
@@ -654,6 +687,7 @@ int64_t upload_seq(DevState& st, const Shard& s, int64_t word_lo, int64_t word_h
         }
         SG_CUDA_CHECK(cudaMemsetAsync(st.ready.as<uint32_t>() + c, 1, 4, cs));
     }
+    SG_CUDA_CHECK(cudaEventRecord(st.copy_done, cs));
     return h2d_bytes;
 }
 
@@ -718,8 +752,6 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
     const long long rounds = std::max(1LL, (static_cast<long long>(n) + max_lanes - 1) / max_lanes);
     const long long lanes_needed = (static_cast<long long>(n) + rounds - 1) / rounds;
     long long grid = (lanes_needed + 32LL * wpb - 1) / (32LL * wpb);
-    if (const char* e = getenv("SG_MAX_BLOCKS")) grid = std::min(grid, atoll(e));  // experiments
-    if (const char* e = getenv("SG_BLOCKS")) grid = std::max(1LL, std::min(atoll(e), max_grid));
     return std::max(1LL, std::min(grid, max_grid));
 }
 
@@ -731,8 +763,7 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
 long long band_active_warps(const DevState& st, const RunConfig& rc, int64_t n) {
     (void)rc;
     const long long max_warps = static_cast<long long>(st.sms) * sgk::mixed_band_warps();
-    long long w = (static_cast<long long>(n) + 31) / 32;
-    if (const char* e = getenv("SG_BAND_WARPS")) w = atoll(e);  // experiments
+    const long long w = (static_cast<long long>(n) + 31) / 32;
     return std::max(1LL, std::min(w, max_warps));
 }
 
@@ -817,24 +848,19 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     p.wcap = rc.wcap;
     p.phase_cycles = nullptr;
     p.warp_times = nullptr;
-    if (const char* e = getenv("SG_WARP_TIMES")) {  // diagnostics
-        if (e[0] == '1') {
-            static unsigned long long* wbuf = nullptr;
-            if (!wbuf) SG_CUDA_CHECK(cudaMalloc(&wbuf, 8 * 3 * 8192));
-            SG_CUDA_CHECK(cudaMemsetAsync(wbuf, 0, 8 * 3 * 8192, st.stream));
-            p.warp_times = wbuf;
-            g_warp_times = wbuf;
-            g_warp_count = static_cast<int>(rc.band ? grid_band * 9 : grid * wpb);
-        }
+    st.diag_flags = options().diagnostics;
+    if (st.diag_flags & SG_DIAG_WARP_TIMES) {
+        st.diag_warps = static_cast<int>(std::min<long long>(
+            8192, rc.band ? grid_band * sgk::mixed_warps_per_block()
+                          : grid * wpb));
+        st.diag_warp.ensure(8 * 3 * 8192);
+        SG_CUDA_CHECK(cudaMemsetAsync(st.diag_warp.p, 0, 8 * 3 * 8192, st.stream));
+        p.warp_times = st.diag_warp.as<unsigned long long>();
     }
-    if (const char* e = getenv("SG_PHASE_CYCLES")) {
-        if (e[0] == '1') {
-            static unsigned long long* dbuf = nullptr;
-            if (!dbuf) SG_CUDA_CHECK(cudaMalloc(&dbuf, 256));
-            SG_CUDA_CHECK(cudaMemsetAsync(dbuf, 0, 256, st.stream));
-            p.phase_cycles = dbuf;
-            g_phase_buf = dbuf;
-        }
+    if (st.diag_flags & SG_DIAG_PHASE_CYCLES) {
+        st.diag_phase.ensure(256);
+        SG_CUDA_CHECK(cudaMemsetAsync(st.diag_phase.p, 0, 256, st.stream));
+        p.phase_cycles = st.diag_phase.as<unsigned long long>();
     }
 
     int launches = 0;
@@ -865,13 +891,6 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         p.u_count = st.mixed_ctr.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
-        if (getenv("SG_BAND_DEBUG")) {  // development aid: how many pairs K0 diverted
-            unsigned cnt = 0;
-            SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
-            SG_CUDA_CHECK(cudaMemcpy(&cnt, p.u_count, 4, cudaMemcpyDeviceToHost));
-            std::fprintf(stderr, "[sg band] %u of %lld pairs to the full-frame K1\n", cnt,
-                         static_cast<long long>(n));
-        }
         sgk::AlignParams pu = p;
         pu.warp_times = nullptr;
         pu.mixed = 0;
@@ -889,6 +908,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         ++launches;
     }
     SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
+    // trailing pieces of a streamed upload no pair waited for finish before the call does
+    SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.copy_done, 0));
     SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_offsets(
         st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), static_cast<int32_t>(n),
         st.scan_tmp.p, st.scan_tmp.cap, st.stream)));
@@ -983,9 +1004,175 @@ void finish_totals(sg_results* out) {
         for (int c = 0; c < SG_CNT_COUNT; ++c) out->total[c] += out->counters[k * SG_CNT_COUNT + c];
 }
 
+// ------------------------------------------------------------ K5: shards over devices
+
+// Estimated alignment cost of a pair for the device split: its length times the
+// rows per window. An unrelated pair (cfg5's independent 30 %) runs ~36 rows per
+// window against ~8 for a correlated read, ~4.7x the work.
+constexpr float kUnrelatedCost = 4.7f;
+
+// How the pairs of one call go to the devices. Pairs are
+// independent, so there is no exchange and no collective: each device aligns its
+// shard and the host puts the results back in input order (batch.cpp:28,45).
+//  * one device, or pairs of near-equal length and relatedness (cfg2/3/4): contiguous
+//    ranges of input order with balanced estimated cost, read in place;
+//  * otherwise (cfg5's mix of 100..20k bp, 30 % unrelated): the pairs are sorted
+//    into cost buckets (4 per octave, longest first, input order inside a bucket)
+//    and dealt longest-processing-time-first to the least-loaded device; each
+//    device's members are gathered into one packed batch, and the permutation
+//    puts the results back.
+struct ShardPlan {
+    std::vector<int64_t> cut;                   // contiguous: shard d = [cut[d], cut[d+1])
+    std::vector<std::vector<int64_t>> members;  // gathered: input indices of shard d, in order
+    bool gathered = false;
+};
+
+ShardPlan plan_shards(const sg_packed_pairs* in, size_t nd) {
+    ShardPlan plan;
+    const int64_t n = in->n_pairs;
+    plan.cut.assign(nd + 1, n);
+    plan.cut[0] = 0;
+    if (nd == 1 || n == 0) return plan;
+    std::vector<float> cost(static_cast<size_t>(n));
+    std::atomic<int64_t> unrelated{0};
+    parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+        int64_t u = 0;
+        for (int64_t k = lo; k < hi; ++k) {
+            const bool rel = pair_related(in, k, 128, 1);
+            u += !rel;
+            cost[static_cast<size_t>(k)] =
+                static_cast<float>(in->text_len[k] + in->pat_len[k]) * (rel ? 1.f : kUnrelatedCost);
+        }
+        unrelated += u;
+    }, 4096);
+    const auto mm = std::minmax_element(cost.begin(), cost.end());
+    if (*mm.second <= 1.25f * *mm.first) {
+        double total = 0;
+        for (float c : cost) total += c;
+        double acc = 0;
+        size_t d = 1;
+        for (int64_t k = 0; k < n && d < nd; ++k) {
+            acc += cost[static_cast<size_t>(k)];
+            while (d < nd && acc * static_cast<double>(nd) >= total * static_cast<double>(d))
+                plan.cut[d++] = k + 1;
+        }
+        return plan;
+    }
+    plan.gathered = true;
+    // buckets: 4 per octave of estimated cost, most expensive first (stable counting sort)
+    constexpr int kBuckets = 4 * 40;
+    std::vector<int> bucket(static_cast<size_t>(n));
+    std::vector<int64_t> start(kBuckets + 1, 0);
+    for (int64_t k = 0; k < n; ++k) {
+        const int b = std::min(kBuckets - 1, std::max(0, static_cast<int>(4.0f * std::log2(
+                                                      std::max(1.0f, cost[static_cast<size_t>(k)])))));
+        bucket[static_cast<size_t>(k)] = kBuckets - 1 - b;
+        ++start[static_cast<size_t>(kBuckets - b)];
+    }
+    for (int b = 0; b < kBuckets; ++b) start[b + 1] += start[b];
+    std::vector<int64_t> sorted(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) sorted[static_cast<size_t>(start[bucket[static_cast<size_t>(k)]]++)] = k;
+    // LPT over the bucket order
+    plan.members.assign(nd, {});
+    std::vector<double> load(nd, 0.0);
+    for (int64_t k : sorted) {
+        const size_t d = static_cast<size_t>(std::min_element(load.begin(), load.end()) - load.begin());
+        plan.members[d].push_back(k);
+        load[d] += cost[static_cast<size_t>(k)];
+    }
+    return plan;
+}
+
+// Copies `len` bases starting at base `off` of src into dst from its base 0.
+void copy_bases(const uint32_t* src, int64_t src_words, int64_t off, int64_t len, uint32_t* dst) {
+    const int64_t words = (len + 15) / 16;
+    const int64_t w0 = off >> 4;
+    const int sh = static_cast<int>(2 * (off & 15));
+    if (sh == 0) {
+        std::memcpy(dst, src + w0, 4 * static_cast<size_t>(words));
+    } else {
+        for (int64_t w = 0; w < words; ++w) {
+            const uint32_t lo = src[w0 + w] >> sh;
+            const uint32_t hi = w0 + w + 1 < src_words ? src[w0 + w + 1] << (32 - sh) : 0u;
+            dst[w] = lo | hi;
+        }
+    }
+    if (len & 15) dst[words - 1] &= (1u << (2 * (len & 15))) - 1u;
+}
+
+// Packs the members of a gathered shard into one batch (pinned, word-aligned).
+void gather_shard(const sg_packed_pairs* in, const std::vector<int64_t>& mem, Packed& pk) {
+    const int64_t n = static_cast<int64_t>(mem.size());
+    std::vector<int64_t> tl(static_cast<size_t>(n)), pl(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+        tl[static_cast<size_t>(k)] = in->text_len[mem[static_cast<size_t>(k)]];
+        pl[static_cast<size_t>(k)] = in->pat_len[mem[static_cast<size_t>(k)]];
+    }
+    layout_offsets(pk, n, tl.data(), pl.data());
+    uint32_t* seq = pk.seq.as<uint32_t>();
+    const int64_t* to = pk.text_off.as<int64_t>();
+    const int64_t* po = pk.pat_off.as<int64_t>();
+    std::vector<uint8_t> hn(static_cast<size_t>(n), 0);
+    bool any_n = false;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t g = mem[static_cast<size_t>(k)];
+        copy_bases(in->seq, in->seq_words, in->text_off[g], in->text_len[g], seq + to[k] / 16);
+        copy_bases(in->seq, in->seq_words, in->pat_off[g], in->pat_len[g], seq + po[k] / 16);
+        if (in->nmask && (any_bits(in->nmask, in->text_off[g], in->text_len[g]) ||
+                          any_bits(in->nmask, in->pat_off[g], in->pat_len[g]))) {
+            hn[static_cast<size_t>(k)] = 1;
+            any_n = true;
+        }
+    }
+    pk.any_n = any_n;
+    if (!any_n) return;
+    const size_t nm_words = static_cast<size_t>((pk.seq_words * 16 + 31) / 32 + 2);
+    pk.nmask.ensure(4 * nm_words);
+    uint32_t* nm = pk.nmask.as<uint32_t>();
+    std::memset(nm, 0, 4 * nm_words);
+    auto copy_bits = [&](int64_t src, int64_t len, int64_t dst) {
+        for (int64_t i = 0; i < len; ++i)
+            if ((in->nmask[(src + i) >> 5] >> ((src + i) & 31)) & 1u)
+                nm[(dst + i) >> 5] |= 1u << ((dst + i) & 31);
+    };
+    for (int64_t k = 0; k < n; ++k) {
+        if (!hn[static_cast<size_t>(k)]) continue;
+        const int64_t g = mem[static_cast<size_t>(k)];
+        copy_bits(in->text_off[g], in->text_len[g], to[k]);
+        copy_bits(in->pat_off[g], in->pat_len[g], po[k]);
+    }
+}
+
+// All device threads of a call meet here between the kernels and the result copy;
+// the last to arrive runs `on_last` (sizes and allocates the result) for all of them.
+class Rendezvous {
+  public:
+    explicit Rendezvous(size_t n) : count_(n) {}
+    template <class F> void arrive(F&& on_last) {
+        std::unique_lock<std::mutex> lk(mu_);
+        if (++waiting_ == count_) {
+            on_last();
+            done_ = true;
+            cv_.notify_all();
+        } else {
+            cv_.wait(lk, [&] { return done_; });
+        }
+    }
+
+  private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    size_t count_, waiting_ = 0;
+    bool done_ = false;
+};
+
 // ------------------------------------------------------------ batch driver
 
 thread_local int64_t g_last_h2d = 0, g_last_d2h = 0;
+
+double since_ms(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
 
 int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int* devices,
                       int n_devices, sg_results* out) {
@@ -1009,136 +1196,195 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     for (int d = 0; d < n_devices; ++d)
         if (devices[d] < 0 || devices[d] >= count)
             return set_error(SG_CONFIG, "bad device index %d", devices[d]);
+    DeviceGuard guard;
+    const sg_options opt = options();
+    const bool trace = (opt.diagnostics & SG_DIAG_HOST_TRACE) != 0;
     const RunConfig rcfg = run_config(cfg, n, in->text_len, in->pat_len);
     const size_t nd = static_cast<size_t>(n_devices);
+    const ShardPlan plan = plan_shards(in, nd);
+    if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "plan", since_ms(t0));
 
-    // K5: contiguous shards with balanced cost (text + pattern length)
-    std::vector<int64_t> cut(nd + 1, 0);
-    {
-        int64_t total = 0;
-        for (int64_t k = 0; k < n; ++k) total += in->text_len[k] + in->pat_len[k];
-        int64_t acc = 0;
-        size_t d = 1;
-        for (int64_t k = 0; k < n && d < nd; ++k) {
-            acc += in->text_len[k] + in->pat_len[k];
-            while (d < nd && acc * static_cast<int64_t>(nd) >= total * static_cast<int64_t>(d))
-                cut[d++] = k + 1;
-        }
-        while (d < nd) cut[d++] = n;
-        cut[nd] = n;
-    }
     bool mixed = false;
     for (int64_t k = 1; k < n && !mixed; ++k)
         mixed = in->text_len[k] + in->pat_len[k] != in->text_len[0] + in->pat_len[0];
 
     std::vector<ShardOut> so(nd);
     std::vector<ShardPrep> prep(nd);
-    std::vector<std::unique_lock<std::mutex>> locks(nd);
-    std::vector<DevState*> states(nd, nullptr);
+    std::vector<Packed> gathered(plan.gathered ? nd : 0);
+    std::vector<sg_packed_pairs> views(nd);
+    std::vector<PinBuf> stage(nd);  // gathered shards: run bytes before the scatter
+    int fail_code = SG_OK;
+    std::string fail_msg;
+    int64_t run_total = 0;
+    std::vector<int64_t> run_base(nd, 0);
+    Rendezvous meet(nd);
 
-    auto run_phase = [&](auto&& body) {
-        if (nd == 1) {
-            body(0);
+    // Runs once, after every shard's kernels: errors, then the first failing pair
+    // in input order (batch.cpp:94-97), then the result buffers and the CIGAR
+    // offsets in input order.
+    auto size_results = [&]() {
+        for (auto& o : so)
+            if (o.err && !fail_code) {
+                fail_code = o.err;
+                fail_msg = o.msg;
+            }
+        if (fail_code) return;
+        int64_t bad = -1;
+        int32_t bad_status = 0;
+        for (size_t d = 0; d < nd; ++d) {
+            const int64_t sn = plan.gathered ? static_cast<int64_t>(plan.members[d].size())
+                                             : plan.cut[d + 1] - plan.cut[d];
+            const int32_t* st = so[d].status.as<int32_t>();
+            for (int64_t k = 0; k < sn; ++k) {
+                if (!st[k]) continue;
+                const int64_t g = plan.gathered ? plan.members[d][static_cast<size_t>(k)] : plan.cut[d] + k;
+                if (bad < 0 || g < bad) {
+                    bad = g;
+                    bad_status = st[k];
+                }
+                if (!plan.gathered) break;
+            }
+        }
+        if (bad >= 0) {
+            fail_code = set_error(SG_INTERNAL, "pair '%lld': %s", static_cast<long long>(bad),
+                                  status_detail(bad_status));
+            fail_msg = g_last_error;
             return;
         }
-        std::vector<std::thread> th;
-        for (size_t d = 0; d < nd; ++d) th.emplace_back(body, d);
-        for (auto& t : th) t.join();
-    };
-    // phase 1: prep, upload, kernels, small D2H
-    run_phase([&](size_t d) {
-        ShardOut& o = so[d];
+        for (size_t d = 0; d < nd; ++d) {
+            run_base[d] = run_total;
+            run_total += so[d].run_bytes;
+        }
         try {
+            results_alloc(out, n, run_total);
+        } catch (const Fail& f) {
+            fail_code = f.code;
+            fail_msg = g_last_error;
+            return;
+        }
+        if (plan.gathered) {  // CIGAR offsets in input order from the shards' sizes
+            for (size_t d = 0; d < nd; ++d) {
+                const int64_t* doff = so[d].doff.as<int64_t>();
+                const auto& mem = plan.members[d];
+                for (size_t k = 0; k < mem.size(); ++k) out->cigar_off[mem[k] + 1] = doff[k + 1] - doff[k];
+            }
+            out->cigar_off[0] = 0;
+            for (int64_t k = 0; k < n; ++k) out->cigar_off[k + 1] += out->cigar_off[k];
+        }
+    };
+
+    // One host thread per shard runs it from upload to result copy, holding its
+    // device pipeline throughout.
+    auto body = [&](size_t d) {
+        ShardOut& o = so[d];
+        std::unique_lock<std::mutex> slot_lock;
+        DevState* stp = nullptr;
+        auto guarded = [&](auto&& f) {
+            try {
+                f();
+            } catch (const Fail& f) {
+                o.err = f.code;
+                o.msg = g_last_error;
+            } catch (const std::exception& e) {
+                o.err = SG_INTERNAL;
+                o.msg = e.what();
+            } catch (...) {
+                o.err = SG_INTERNAL;
+                o.msg = "unknown exception in the device pipeline";
+            }
+        };
+        guarded([&] {
             SG_CUDA_CHECK(cudaSetDevice(devices[d]));
             int occ = 0;
             for (size_t e = 0; e < d; ++e) occ += devices[e] == devices[d];
             DevSlot& slot = dev_slot(devices[d], occ);
-            locks[d] = std::unique_lock<std::mutex>(slot.mu);
+            slot_lock = std::unique_lock<std::mutex>(slot.mu);
             if (!slot.st) {
                 slot.st = std::make_unique<DevState>();
                 slot.st->init(devices[d]);
             }
             DevState& st = *slot.st;
-            states[d] = &st;
-            const Shard s{in, cut[d], cut[d + 1]};
-            const bool trace = getenv("SG_TRACE") != nullptr;  // development aid
-            auto mark = [&](const char* what) {
-                if (!trace) return;
-                cudaStreamSynchronize(st.stream);
-                std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", what,
-                             std::chrono::duration<double, std::milli>(
-                                 std::chrono::steady_clock::now() - t0).count());
-            };
-            mark("start");
+            stp = &st;
+            Shard s{in, plan.cut[d], plan.cut[d + 1]};
+            if (plan.gathered) {
+                gather_shard(in, plan.members[d], gathered[d]);
+                views[d] = gathered[d].view();
+                s = Shard{&views[d], 0, static_cast<int64_t>(plan.members[d].size())};
+                if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "gather", since_ms(t0));
+            }
             // streamed: the first round of lanes takes pairs from the front of memory
-            const bool streamed = !getenv("SG_NO_STREAM");
+            const bool streamed = opt.stream_upload != 0;
             // the sequence words first: their copy overlaps the host prep below
             int64_t wlo = 0, whi = 0;
             shard_words(s, &wlo, &whi);
             o.h2d_bytes = upload_seq(st, s, wlo, whi, streamed);
             RunConfig rcs = rcfg;
-            rcs.band = rcfg.band && band_pays(in, s.lo, s.hi, rcfg.W, rcfg.O);
+            rcs.band = rcfg.band && band_pays(s.in, s.lo, s.hi, rcfg.W, rcfg.O);
             const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
             prep_shard(s, prep[d], mixed, split);
-            mark("prep");
             o.h2d_bytes += upload_shard(st, s, prep[d], streamed, true);
-            mark("upload");
+            if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "upload", since_ms(t0));
             o.launches = launch_shard(st, rcs, prep[d]);
-            mark("kernels");
             fetch_small(st, prep[d].n, o);
-            mark("fetch");
-        } catch (const Fail& f) {
-            o.err = f.code;
-            o.msg = g_last_error;
-        }
-    });
-    for (auto& o : so)
-        if (o.err) return set_error(o.err, "%s", o.msg.c_str());
-    for (size_t d = 0; d < nd; ++d)  // first failing pair in input order (batch.cpp:94-97)
-        if (so[d].first_bad >= 0)
-            return set_error(SG_INTERNAL, "pair '%lld': %s",
-                             static_cast<long long>(cut[d] + so[d].first_bad),
-                             status_detail(so[d].first_bad_status));
-    int64_t run_total = 0;
-    std::vector<int64_t> run_base(nd);
-    for (size_t d = 0; d < nd; ++d) {
-        run_base[d] = run_total;
-        run_total += so[d].run_bytes;
-    }
-    try {
-        results_alloc(out, n, run_total);
-    } catch (const Fail& f) {
-        return f.code;
-    }
-    // phase 2: run bytes straight into the result buffer
-    run_phase([&](size_t d) {
-        ShardOut& o = so[d];
-        try {
-            SG_CUDA_CHECK(cudaSetDevice(devices[d]));
-            DevState& st = *states[d];
-            if (o.run_bytes) {
-                SG_CUDA_CHECK(cudaMemcpyAsync(out->runs + run_base[d], st.dense.p,
-                                              static_cast<size_t>(o.run_bytes),
-                                              cudaMemcpyDeviceToHost, st.stream));
-                o.d2h_bytes += o.run_bytes;
+            if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "kernels", since_ms(t0));
+        });
+        meet.arrive(size_results);
+        if (fail_code || !stp) return;
+        guarded([&] {
+            DevState& st = *stp;
+            if (plan.gathered) {
+                stage[d].ensure(static_cast<size_t>(std::max<int64_t>(o.run_bytes, 1)));
+                if (o.run_bytes)
+                    SG_CUDA_CHECK(cudaMemcpyAsync(stage[d].p, st.dense.p, static_cast<size_t>(o.run_bytes),
+                                                  cudaMemcpyDeviceToHost, st.stream));
+                SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+                const auto& mem = plan.members[d];
+                const int32_t* dist = o.dist.as<int32_t>();
+                const int32_t* win = o.win.as<int32_t>();
+                const int64_t* doff = o.doff.as<int64_t>();
+                const uint64_t* cnt = o.cnt.as<uint64_t>();
+                const uint8_t* src = stage[d].as<uint8_t>();
+                for (size_t k = 0; k < mem.size(); ++k) {
+                    const int64_t g = mem[k];
+                    out->distance[g] = dist[k];
+                    out->windows[g] = win[k];
+                    out->found[g] = dist[k] >= 0;
+                    std::memcpy(out->runs + out->cigar_off[g], src + doff[k],
+                                static_cast<size_t>(doff[k + 1] - doff[k]));
+                    std::memcpy(out->counters + g * SG_CNT_COUNT, cnt + k * SG_CNT_COUNT,
+                                8 * SG_CNT_COUNT);
+                }
+            } else {
+                if (o.run_bytes)
+                    SG_CUDA_CHECK(cudaMemcpyAsync(out->runs + run_base[d], st.dense.p,
+                                                  static_cast<size_t>(o.run_bytes),
+                                                  cudaMemcpyDeviceToHost, st.stream));
+                scatter_small(out, plan.cut[d], plan.cut[d + 1] - plan.cut[d], run_base[d], o);
+                SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
             }
-            scatter_small(out, cut[d], cut[d + 1] - cut[d], run_base[d], o);
-            SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
-            if (getenv("SG_TRACE"))
-                std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "runs+scat",
-                             std::chrono::duration<double, std::milli>(
-                                 std::chrono::steady_clock::now() - t0).count());
-        } catch (const Fail& f) {
-            o.err = f.code;
-            o.msg = g_last_error;
-        }
-        locks[d].unlock();
-    });
-    for (auto& o : so)
-        if (o.err) {
-            sg_results_free(out);
-            return set_error(o.err, "%s", o.msg.c_str());
-        }
+            o.d2h_bytes += o.run_bytes;
+            if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "results", since_ms(t0));
+        });
+    };
+    if (nd == 1) {
+        body(0);
+    } else {
+        std::vector<std::thread> th;
+        th.reserve(nd);
+        for (size_t d = 0; d < nd; ++d) th.emplace_back(body, d);
+        for (auto& t : th) t.join();
+    }
+    if (!fail_code)
+        for (auto& o : so)
+            if (o.err) {
+                fail_code = o.err;
+                fail_msg = o.msg;
+                break;
+            }
+    if (fail_code) {
+        sg_results_free(out);
+        return set_error(fail_code, "%s", fail_msg.c_str());
+    }
     finish_totals(out);
     g_last_h2d = g_last_d2h = 0;
     for (auto& o : so) {
@@ -1223,6 +1469,26 @@ void sg_config_default(sg_config* cfg) {
 
 int sg_validate_config(const sg_config* cfg) { return validate_cfg(cfg); }
 
+void sg_options_default(sg_options* o) {
+    o->kernel = SG_KERNEL_AUTO;
+    o->stream_upload = 1;
+    o->longest_first = 1;
+    o->diagnostics = 0;
+    o->exact_budget = 0;
+}
+
+int sg_set_options(const sg_options* o) {
+    if (!o) return set_error(SG_CONFIG, "null options");
+    if (o->kernel < SG_KERNEL_AUTO || o->kernel > SG_KERNEL_WIDE)
+        return set_error(SG_CONFIG, "unknown kernel option %d", o->kernel);
+    if (o->exact_budget < 0) return set_error(SG_CONFIG, "negative exact_budget");
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    g_opt = *o;
+    return SG_OK;
+}
+
+void sg_get_options(sg_options* o) { *o = options(); }
+
 int sg_align_packed(const sg_config* cfg, const sg_packed_pairs* pairs, const int* devices,
                     int n_devices, sg_results* out) {
     try {
@@ -1293,9 +1559,11 @@ int64_t sg_cigar_string(const sg_results* res, int64_t k, char* buf, int64_t cap
     static const char kOp[4] = {'=', 'X', 'I', 'D'};
     int64_t pos = 0;
     char tmp[32];
+    // snprintf semantics: the longest prefix that fits, NUL-terminated
     auto put = [&](int op, int64_t len) {
         const int w = snprintf(tmp, sizeof tmp, "%lld%c", static_cast<long long>(len), kOp[op]);
-        if (buf && pos + w < cap) std::memcpy(buf + pos, tmp, static_cast<size_t>(w));
+        if (buf && pos < cap - 1)
+            std::memcpy(buf + pos, tmp, static_cast<size_t>(std::min<int64_t>(w, cap - 1 - pos)));
         pos += w;
     };
     int prev = -1;
@@ -1353,6 +1621,7 @@ int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int de
     if (rc) return rc;
     if (sg_device_count() <= device || device < 0)
         return set_error(SG_CUDA, "no CUDA device %d (the GPU path has no CPU fallback)", device);
+    DeviceGuard guard;
     auto s = std::make_unique<sg_session>();
     try {
         s->cfg = *cfg;
@@ -1375,6 +1644,7 @@ int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int de
 }
 
 int sg_session_run(sg_session* s, float* device_ms, float* k1_ms) {
+    DeviceGuard guard;
     try {
         SG_CUDA_CHECK(cudaSetDevice(s->st.device));
         s->launches = launch_shard(s->st, s->rc, s->prep);
@@ -1394,6 +1664,7 @@ int sg_session_run(sg_session* s, float* device_ms, float* k1_ms) {
 int sg_session_fetch(sg_session* s, sg_results* out) {
     std::memset(out, 0, sizeof *out);
     if (!s->ran) return set_error(SG_INPUT, "session has not run");
+    DeviceGuard guard;
     try {
         SG_CUDA_CHECK(cudaSetDevice(s->st.device));
         ShardOut so;
@@ -1427,23 +1698,56 @@ int sg_session_info(const sg_session* s, int64_t* lanes, int32_t* sms, int32_t* 
 
 int sg_session_kernel(const sg_session* s) { return s->rc.wide ? 2 : s->rc.band ? 1 : 0; }
 
-void sg_session_destroy(sg_session* s) { delete s; }
+void sg_session_destroy(sg_session* s) {
+    DeviceGuard guard;
+    delete s;
+}
 
-/* Diagnostics: per-phase SM cycles summed over warps of the last run with
- * SG_PHASE_CYCLES=1 (setup, DC, TB+advance, iterations, lanes in DC, TB loop
- * trips, TB lane-steps, TB entries). Not part of the ABI
- * header. */
-int sg_debug_warp_times(unsigned long long* out, int cap) {
-    if (!g_warp_times) return -1;
-    const int n = std::min(cap, g_warp_count);
-    cudaMemcpy(out, g_warp_times, 24 * static_cast<size_t>(n), cudaMemcpyDeviceToHost);
+int sg_session_warp_times(sg_session* s, uint64_t* out, int cap) {
+    if (!s || !(s->st.diag_flags & SG_DIAG_WARP_TIMES) || !s->st.diag_warp.p) return -1;
+    DeviceGuard guard;
+    cudaSetDevice(s->st.device);
+    const int n = std::min(cap, s->st.diag_warps);
+    if (cudaMemcpy(out, s->st.diag_warp.p, 24 * static_cast<size_t>(n), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return -1;
     return n;
 }
 
-int sg_debug_phase_cycles(unsigned long long* out8) {
-    if (!g_phase_buf) return -1;
-    cudaMemcpy(out8, g_phase_buf, 25 * 8, cudaMemcpyDeviceToHost);
+int sg_session_phase_cycles(sg_session* s, uint64_t* out25) {
+    if (!s || !(s->st.diag_flags & SG_DIAG_PHASE_CYCLES) || !s->st.diag_phase.p) return -1;
+    DeviceGuard guard;
+    cudaSetDevice(s->st.device);
+    if (cudaMemcpy(out25, s->st.diag_phase.p, 25 * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
     return 0;
+}
+
+int sg_plan_shards(const sg_packed_pairs* pairs, int n_devices, int32_t* shard, int64_t* pos,
+                   int* gathered) {
+    if (!pairs || pairs->n_pairs < 0 || !shard || !pos) return set_error(SG_INPUT, "null argument");
+    if (n_devices < 1) return set_error(SG_CONFIG, "n_devices must be >= 1");
+    try {
+        const ShardPlan plan = plan_shards(pairs, static_cast<size_t>(n_devices));
+        for (int d = 0; d < n_devices; ++d) {
+            if (plan.gathered) {
+                const auto& mem = plan.members[static_cast<size_t>(d)];
+                for (size_t k = 0; k < mem.size(); ++k) {
+                    shard[mem[k]] = d;
+                    pos[mem[k]] = static_cast<int64_t>(k);
+                }
+            } else {
+                for (int64_t k = plan.cut[static_cast<size_t>(d)]; k < plan.cut[static_cast<size_t>(d) + 1]; ++k) {
+                    shard[k] = d;
+                    pos[k] = k - plan.cut[static_cast<size_t>(d)];
+                }
+            }
+        }
+        if (gathered) *gathered = plan.gathered ? 1 : 0;
+        return SG_OK;
+    } catch (const std::exception& e) {
+        return set_error(SG_INTERNAL, "%s", e.what());
+    }
 }
 
 int64_t sg_last_transfer_bytes(int direction) { return direction ? g_last_d2h : g_last_h2d; }
@@ -1465,6 +1769,7 @@ int sg_global_align(const sg_packed_pairs* pairs, int device, sg_results* out) {
     }
     if (device < 0 || sg_device_count() <= device)
         return set_error(SG_CUDA, "no CUDA device %d (the GPU path has no CPU fallback)", device);
+    DeviceGuard guard;
     try {
         SG_CUDA_CHECK(cudaSetDevice(device));
         DevSlot& slot = dev_slot(device, 0);
@@ -1487,11 +1792,11 @@ int sg_global_align(const sg_packed_pairs* pairs, int device, sg_results* out) {
         st.scan_tmp.ensure(sgk::cigar_offsets_temp_bytes(static_cast<int32_t>(n)) + 64);
         // The delta store (16 B per 32 cells) goes in batches of pairs within a
         // memory budget: half the free device memory (at least 4 GiB), or
-        // SG_EXACT_BUDGET bytes; a pair larger than the budget runs alone.
+        // sg_options.exact_budget bytes; a pair larger than the budget runs alone.
         size_t free_b = 0, total_b = 0;
         SG_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
         int64_t budget = std::max<int64_t>(int64_t{4} << 30, static_cast<int64_t>(free_b / 2));
-        if (const char* e = getenv("SG_EXACT_BUDGET")) budget = std::max<int64_t>(1, atoll(e));
+        if (const int64_t b = options().exact_budget) budget = b;
         PinBuf soff, hoff;
         soff.ensure(8 * n1);
         hoff.ensure(8 * n1);

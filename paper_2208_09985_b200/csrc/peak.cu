@@ -36,8 +36,7 @@ __global__ void __launch_bounds__(256) k_lop3_peak(unsigned* out, int iters, lon
 
 }  // namespace
 
-extern "C" int sg_alu_peak(int device, double* ops_per_clk_per_sm, double* sm_mhz,
-                           double* ops_per_s) {
+static int alu_peak(int device, double* ops_per_clk_per_sm, double* sm_mhz, double* ops_per_s) {
     if (cudaSetDevice(device) != cudaSuccess) return SG_CUDA;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -71,4 +70,13 @@ extern "C" int sg_alu_peak(int device, double* ops_per_clk_per_sm, double* sm_mh
     if (sm_mhz) *sm_mhz = maxc / (ms * 1e-3) / 1e6;
     if (ops_per_s) *ops_per_s = ops / (ms * 1e-3);
     return SG_OK;
+}
+
+extern "C" int sg_alu_peak(int device, double* ops_per_clk_per_sm, double* sm_mhz,
+                           double* ops_per_s) {
+    int prev = -1;  // the caller's current device is restored
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    const int rc = alu_peak(device, ops_per_clk_per_sm, sm_mhz, ops_per_s);
+    if (prev >= 0) cudaSetDevice(prev);
+    return rc;
 }

@@ -2207,6 +2207,7 @@ int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint
 
 int mixed_band_warps() { return band::WARPS; }
 int mixed_full_warps() { return band::FWARPS; }
+int mixed_warps_per_block() { return kMixedWarps; }
 
 int mixed_max_blocks_per_sm(int LF) {
     int blocks = 0;

@@ -125,6 +125,7 @@ int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint
 
 int mixed_band_warps();
 int mixed_full_warps();
+int mixed_warps_per_block();  // band + full-frame + cooperative warps
 int mixed_max_blocks_per_sm(int LF);
 bool band_eligible(int W, int O, int single);
 

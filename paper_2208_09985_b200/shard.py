@@ -1,12 +1,18 @@
 """Multi-GPU plumbing for the benchmark and batch drivers (K5).
 
-Pairs are independent: no data-path collective. A
-rank aligns its own contiguous slice; torch.distributed is used only for the
-barrier and the max-over-ranks timing.
+Pairs are independent: no data-path collective. Under
+torchrun a rank aligns its own contiguous slice of the generator (weak scaling);
+in one process, sg_align_packed(devices=[...]) splits a batch with the C++ plan
+that `plan` exposes (host.cu plan_shards). torch.distributed is used
+only for the barrier and the max-over-ranks timing.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
+
+from . import _ffi
 
 
 def rank_range(rank: int, world: int, per_rank: int):
@@ -16,26 +22,25 @@ def rank_range(rank: int, world: int, per_rank: int):
     return rank * per_rank, per_rank
 
 
-def cost_cuts(lengths, parts: int):
-    """Contiguous shards of balanced cost (text+pattern length); mirrors the C ABI's
-    device split (host.cu align_packed_impl). Returns parts+1 cut indices."""
-    lengths = np.asarray(lengths, dtype=np.int64)
-    n = len(lengths)
-    cuts = np.zeros(parts + 1, dtype=np.int64)
-    total = int(lengths.sum())
-    acc = np.cumsum(lengths)
-    d = 1
-    for k in range(n):
-        while d < parts and acc[k] * parts >= total * d:
-            cuts[d] = k + 1
-            d += 1
-        if d >= parts:
-            break
-    while d < parts:
-        cuts[d] = n
-        d += 1
-    cuts[parts] = n
-    return cuts
+def plan(batch, n_devices: int):
+    """The library's device split of a PackedBatch (sg_plan_shards): per pair its
+    device slot and its position in that device's batch, and whether the shards
+    are gathered (cost buckets + longest-first) or contiguous ranges."""
+    from .aligner import _check
+    n = batch.n
+    shard = np.zeros(max(n, 1), np.int32)
+    pos = np.zeros(max(n, 1), np.int64)
+    gathered = C.c_int()
+    _check(_ffi.load().sg_plan_shards(C.byref(batch.c), n_devices,
+                                      shard.ctypes.data_as(C.c_void_p),
+                                      pos.ctypes.data_as(C.c_void_p), C.byref(gathered)))
+    return shard[:n], pos[:n], bool(gathered.value)
+
+
+def members(shard, pos, d: int):
+    """Input indices of device slot d's pairs, in that device's order."""
+    idx = np.nonzero(shard == d)[0]
+    return idx[np.argsort(pos[idx], kind="stable")]
 
 
 def max_over_ranks(value: float, device=None) -> float:

@@ -49,10 +49,10 @@ for (W, O) in ((64, 24), (64, 33), (48, 16), (60, 20), (36, 12)):
     for (s_, d_, e_) in ((1, 1, 1), (0, 0, 0), (1, 0, 1)):
         cfg = sg.AlignerConfig(W=W, O=O, sene=bool(s_), dent=bool(d_), early_termination=bool(e_))
         res = {}
-        for fr in ("band", "full"):
-            os.environ["SG_FRAME"] = fr
+        for fr, kern in (("band", "mixed"), ("full", "full")):
             try:
-                res[fr] = sg.align_codes(cfg, batch)
+                with sg.options(kernel=kern):
+                    res[fr] = sg.align_codes(cfg, batch)
             except Exception as ex:
                 res[fr] = ex
         a, b = res["band"], res["full"]

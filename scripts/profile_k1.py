@@ -11,19 +11,20 @@ ap.add_argument("--W", type=int, default=64)
 ap.add_argument("--O", type=int, default=24)
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--phases", action="store_true", help="per-phase cycle counters")
+ap.add_argument("--kernel", default="auto")
 a = ap.parse_args()
 batch = sg.synth_packed(a.cfg, a.seed, a.pairs)
-s = sg.Session(sg.AlignerConfig(W=a.W, O=a.O), batch)
+with sg.options(kernel=a.kernel):
+    s = sg.Session(sg.AlignerConfig(W=a.W, O=a.O), batch)
 for _ in range(a.runs):
-    ms, k1 = s.run()
+    with sg.options(kernel=a.kernel, diagnostics=2 if a.phases else 0):
+        ms, k1 = s.run()
     print(f"cfg{a.cfg} pairs={a.pairs} K1-K3 {ms:.3f} ms  K1 {k1:.3f} ms  {a.pairs / (ms / 1e3):.0f} aln/s  {s.info()}", flush=True)
 r = s.fetch()
 print("cells_computed", r.total.cells_computed, "ALG_OPS/s (K1)", 4 * ((a.W + 31) // 32) * r.total.cells_computed / (k1 / 1e3) / 1e12, "T")
-if os.environ.get("SG_PHASE_CYCLES") == "1":
-    import ctypes as C
-    from paper_2208_09985_b200 import _ffi
-    buf = (C.c_ulonglong * 25)()
-    _ffi.load().sg_debug_phase_cycles(buf)
+if a.phases:
+    buf = s.phase_cycles()
     for name, o in (("band/K1", 0), ("full", 9)):
         b = buf[o:o + 9]
         tot = b[0] + b[1] + b[2] + b[8]

@@ -1,8 +1,7 @@
-"""When each warp of the mixed K1 last had work (SG_WARP_TIMES=1): the end of the
+"""When each warp of the mixed K1 last had work (options(diagnostics=1)): the end of the
 batch by role (7 band + 2 cooperative warps per block). Development aid.
 usage: warp_last_busy.py [cfg] [pairs] [W] [O]"""
 import ctypes as C, os, sys
-os.environ["SG_WARP_TIMES"] = "1"
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import paper_2208_09985_b200 as sg
@@ -12,11 +11,10 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
 W = int(sys.argv[3]) if len(sys.argv) > 3 else 64; O = int(sys.argv[4]) if len(sys.argv) > 4 else 24
 batch = sg.synth_packed(cfg, 0, n)
 s = sg.Session(sg.AlignerConfig(W=W, O=O), batch)
-s.run(); ms, k1 = s.run()
-lib = _ffi.load()
-lib.sg_debug_warp_times.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * (3 * 8192))()
-cnt = lib.sg_debug_warp_times(buf, 8192)
+with sg.options(diagnostics=1):
+    s.run(); ms, k1 = s.run()
+buf = (C.c_uint64 * (3 * 8192))()
+cnt = _ffi.load().sg_session_warp_times(s._h, buf, 8192)
 a = np.frombuffer(buf, dtype=np.uint64)[: 3 * cnt].reshape(cnt, 3).astype(np.int64)
 idx = np.arange(cnt); wib = idx % 9
 ok = a[:, 0] > 0

@@ -1,7 +1,6 @@
-"""Per-warp exit times of one K1 launch (SG_WARP_TIMES=1): how the batch tail
+"""Per-warp exit times of one K1 launch (options(diagnostics=1)): how the batch tail
 drains (development aid)."""
 import ctypes as C, os, sys
-os.environ["SG_WARP_TIMES"] = "1"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
@@ -10,11 +9,10 @@ from paper_2208_09985_b200 import _ffi
 pairs = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 batch = sg.synth_packed(3, 0, pairs)
 s = sg.Session(sg.AlignerConfig(W=64, O=24), batch)
-s.run(); ms, k1 = s.run()
-lib = _ffi.load()
-lib.sg_debug_warp_times.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
-buf = (C.c_ulonglong * (3 * 8192))()
-n = lib.sg_debug_warp_times(buf, 8192)
+with sg.options(diagnostics=1):
+    s.run(); ms, k1 = s.run()
+buf = (C.c_uint64 * (3 * 8192))()
+n = _ffi.load().sg_session_warp_times(s._h, buf, 8192)
 a = np.frombuffer(buf, dtype=np.uint64)[: 3 * n].reshape(n, 3).astype(np.int64)
 t0 = a[:, 0].min(); start = (a[:, 0] - t0) / 1e6; end = (a[:, 1] - t0) / 1e6; sm = a[:, 2]
 print(f"K1 {k1:.2f} ms, warps {n}, start spread {start.max():.3f} ms")

@@ -94,3 +94,46 @@ def single_files():
         m = _SINGLE.search(path)
         out.append((os.path.basename(path), int(m.group(2)), int(m.group(3)), int(m.group(4))))
     return out
+
+
+_DIGEST = re.compile(r"(cfg\d)(?:_W(\d+)_O(\d+)_s(\d)d(\d)e(\d))?\.tsv$")
+
+
+def digest_files():
+    """(file, cfg_id, W, O, sene, dent, et) of every whole-config digest file
+    (tests/golden/make_digests.py)."""
+    out = []
+    for path in sorted(glob.glob(os.path.join(HERE, "digests", "cfg*.tsv"))):
+        m = _DIGEST.search(path)
+        cfg = int(m.group(1)[3:])
+        if m.group(2):
+            W, O, s, d, e = (int(m.group(k)) for k in range(2, 7))
+        else:
+            W, O, s, d, e = 64, 24, 1, 1, 1
+        out.append((os.path.basename(path), cfg, W, O, s, d, e))
+    return out
+
+
+def read_digests(name):
+    """-> (blocks [(first, count, hex)], total_pairs, total_hex, total_cells)."""
+    blocks, total = [], None
+    with open(os.path.join(HERE, "digests", name)) as f:
+        for line in f:
+            parts = line.rstrip("\n").split("\t")
+            if parts[0] == "total":
+                total = (int(parts[1]), parts[2], int(parts[3]))
+            else:
+                blocks.append((int(parts[0]), int(parts[1]), parts[2]))
+    assert total is not None, name
+    return blocks, total[0], total[1], total[2]
+
+
+def fnv1a_bytes(b: bytes, h: int = 1469598103934665603) -> int:
+    for ch in b:
+        h = ((h ^ ch) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def digest_total(block_hex):
+    """The digest file's total: fnv1a64 over the blocks' 16-hex-digit forms."""
+    return f"{fnv1a_bytes(''.join(block_hex).encode()):016x}"

@@ -81,6 +81,9 @@ def lib():
         L.orc_score_cigar.restype = C.c_int64
         L.orc_worst_quantile.argtypes = [C.POINTER(C.c_int64), C.c_int64, C.c_double]
         L.orc_worst_quantile.restype = C.c_int64
+        L.orc_digest_blocks.argtypes = [C.c_int64] + [C.c_void_p] * 6 + [C.c_int64, C.c_void_p,
+                                                                          C.c_int]
+        L.orc_digest_blocks.restype = C.c_uint64
         _lib = L
     return _lib
 
@@ -199,3 +202,45 @@ def replay_batch(codes, results, threads=None) -> int:
                                       ptr(codes.pat_len), ptr(results.runs),
                                       ptr(results.cigar_off), ptr(dist),
                                       threads or (os.cpu_count() or 8)))
+
+
+def digest_blocks(distance, windows, found, cigar_off, runs, counters, block=1000, threads=None):
+    """Per-block digests of a batch's results (orc_digest_blocks; the same records as
+    `ref_tool digest`, oracle/ref_tool.cpp:digest_line) -> (list of hex, total hex)."""
+    import numpy as np
+    n = len(distance)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    dist = np.ascontiguousarray(distance, dtype=np.int64)
+    win = np.ascontiguousarray(windows, dtype=np.int32)
+    fnd = None if found is None else np.ascontiguousarray(found, dtype=np.uint8)
+    off = np.ascontiguousarray(cigar_off, dtype=np.int64)
+    rb = np.ascontiguousarray(runs, dtype=np.uint8)
+    if rb.size == 0:
+        rb = np.zeros(1, np.uint8)
+    cnt = np.ascontiguousarray(counters, dtype=np.uint64).reshape(-1)
+    out = np.zeros(max(1, (n + block - 1) // block), np.uint64)
+    total = lib().orc_digest_blocks(n, ptr(dist), ptr(win), None if fnd is None else ptr(fnd),
+                                    ptr(off), ptr(rb), ptr(cnt), block, ptr(out),
+                                    threads or os.cpu_count() or 8)
+    return [f"{int(x):016x}" for x in out[: (n + block - 1) // block]], f"{total:016x}"
+
+
+def results_digests(res, block=1000):
+    """digest_blocks over a paper_2208_09985_b200 Results object."""
+    return digest_blocks(res.distance, res.windows, res.found, res.cigar_off, res.runs,
+                         res.counters, block)
+
+
+def runs_from_cigar(cigar: str) -> bytes:
+    """The GPU path's run-byte encoding ((op << 6) | (len - 1), <= 64 per byte) of a
+    CIGAR string; used to pin the digest over run bytes without a GPU."""
+    import re
+    out = bytearray()
+    for n, op in re.findall(r"(\d+)([=XID])", cigar):
+        n = int(n)
+        code = "=XID".index(op)
+        while n > 0:
+            k = min(n, 64)
+            out.append((code << 6) | (k - 1))
+            n -= k
+    return bytes(out)

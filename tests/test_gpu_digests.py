@@ -1,0 +1,45 @@
+"""EVERY pair of every BASELINE config, bit-exact against the reference on the GPU.
+
+tests/golden/digests/ holds, per config and (W, O, switch) setting, an FNV-1a-64
+digest of each block of 1,000 pairs' reference results — distance, CIGAR hash, run
+count, windows and all 7 InstrumentationCounters (make_digests.py, from the
+unmodified run_batch, proj/src/batch.cpp:13-104). This test aligns the whole config
+on the GPU (cfg1 10k, cfg2 1M, cfg3 100k, cfg4 20k at 4 (W, O) x 8 switch
+combinations, cfg5 500k pairs) and recomputes every block digest from the results
+(orc_digest_blocks, pinned on the CPU by test_digests.py). It runs each config with
+the host's choice of K1 kernel and again with the mixed kernel forced, so both K1
+kernels are checked on every pair (the reference's contract: identical output for
+every pair, proj/tests/acceptance.cpp:93-126, :258-281).
+"""
+import pytest
+
+import golden_io as G
+import oracle_ffi as O
+
+pytestmark = pytest.mark.gpu
+
+_BATCH = {}
+
+
+def _batch(sg, cfg_id):
+    if cfg_id not in _BATCH:
+        _BATCH.clear()  # one config resident at a time (cfg5 is ~1 GB packed)
+        _BATCH[cfg_id] = sg.synth_packed(cfg_id)
+    return _BATCH[cfg_id]
+
+
+@pytest.mark.parametrize("kernel", ["auto", "mixed"])
+@pytest.mark.parametrize("name,cfg,W,Ov,s,d,e", G.digest_files())
+def test_whole_config_digests(gpu, name, cfg, W, Ov, s, d, e, kernel):
+    sg = gpu
+    blocks, pairs, total, cells = G.read_digests(name)
+    batch = _batch(sg, cfg)
+    assert batch.n == pairs
+    config = sg.AlignerConfig(W=W, O=Ov, sene=bool(s), dent=bool(d), early_termination=bool(e))
+    with sg.options(kernel=kernel):
+        res = sg.align_packed(config, batch)
+    assert int(res.total.cells_computed) == cells
+    got, tot = O.results_digests(res)
+    bad = [(b0, cnt) for (b0, cnt, want), have in zip(blocks, got) if want != have]
+    assert not bad, f"{name} [{kernel}]: {len(bad)} of {len(blocks)} blocks differ, first {bad[:5]}"
+    assert tot == total

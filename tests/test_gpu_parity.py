@@ -22,12 +22,12 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(params=["auto", "band"])
-def frame(request, monkeypatch):
+def frame(request, set_options):
     """Runs a test with the host's choice of K1 kernel and again with the mixed
     band-frame kernel forced: small or short-read batches
     otherwise go to the full-frame K1 (host.cu band_pays)."""
     if request.param == "band":
-        monkeypatch.setenv("SG_FRAME", "band")
+        set_options(kernel="mixed")
     return request.param
 
 
@@ -154,12 +154,12 @@ WIDE_CROSS = ["kat_W64_O33.tsv", "kat_W16_O0.tsv", "kat_W1_O0.tsv", "kat_W65_O33
 
 
 @pytest.mark.parametrize("name", WIDE_CROSS)
-def test_wide_kernel_on_narrow_windows(gpu, monkeypatch, name):
+def test_wide_kernel_on_narrow_windows(gpu, set_options, name):
     """K6 (csrc/wide_align.cu) forced onto windows K1 normally takes: the same
-    reference fixtures must come out (SG_FORCE_WIDE=1 is read per call)."""
+    reference fixtures must come out (sg_options.kernel = SG_KERNEL_WIDE)."""
     sg = gpu
     W, Ov, s, d, e = next(f[1:] for f in G.kat_files() if f[0] == name)
-    monkeypatch.setenv("SG_FORCE_WIDE", "1")
+    set_options(kernel="wide")
     pairs = G.kat_pairs()
     rows = G.read_golden(name)
     codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
@@ -318,14 +318,14 @@ def test_single_window_run_batch_and_tsv(gpu):
 
 
 @pytest.mark.gpu
-def test_mixed_handoffs_terminate(gpu, monkeypatch):
+def test_mixed_handoffs_terminate(gpu, set_options):
     """K1 mixed: a window the band frame fails on (D > 30) must
     not bounce between the warp roles. For W < 64 a window can be both band- and
     STD-shaped; the W = 32 KATs hit that case (one of them looped for minutes
     when the band frame could take such a window back)."""
     import time
     sg = gpu
-    monkeypatch.setenv("SG_FRAME", "band")
+    set_options(kernel="mixed")
     pairs = G.kat_pairs()
     rows = G.read_golden("kat_W32_O17.tsv")
     codes = sg.CodesBatch.from_lists([sg.encode_sequence(pairs[r["id"]][0]) for r in rows],
@@ -389,7 +389,7 @@ def _stress_batch(sg, seed, n):
 
 
 @pytest.mark.parametrize("W,Ov,s,d,e", [(64, 24, 1, 1, 1), (64, 33, 0, 0, 0), (48, 16, 1, 0, 1)])
-def test_mixed_kernel_matches_full_frame(gpu, monkeypatch, W, Ov, s, d, e):
+def test_mixed_kernel_matches_full_frame(gpu, W, Ov, s, d, e):
     """K1 mixed (band + STD + cooperative warps, queues, K0 routing) against the
     full-frame K1 on a randomized batch: every distance, CIGAR, window count and
     counter identical; a sample is also checked against the oracle."""
@@ -397,9 +397,9 @@ def test_mixed_kernel_matches_full_frame(gpu, monkeypatch, W, Ov, s, d, e):
     texts, pats = _stress_batch(sg, W * 7 + Ov, 4000)
     codes = sg.CodesBatch.from_lists(texts, pats)
     res = {}
-    for fr in ("band", "full"):
-        monkeypatch.setenv("SG_FRAME", fr)
-        res[fr] = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
+    for fr, kernel in (("band", "mixed"), ("full", "full")):
+        with sg.options(kernel=kernel):
+            res[fr] = sg.align_codes(_cfg(sg, W, Ov, s, d, e), codes)
     a, b = res["band"], res["full"]
     assert np.array_equal(np.asarray(a.distance), np.asarray(b.distance))
     assert np.array_equal(np.asarray(a.windows), np.asarray(b.windows))

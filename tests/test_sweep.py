@@ -189,10 +189,9 @@ def test_gpu_global_align_random_against_oracle(gpu, monkeypatch):
         texts.append(a)
         pats.append(b)
     batch = sg.pack(sg.CodesBatch.from_lists(texts, pats))
-    for budget in (None, "1"):
-        if budget:
-            monkeypatch.setenv("SG_EXACT_BUDGET", budget)
-        res = sg.global_align_packed(batch)
+    for budget in (None, 1):
+        with sg.options(exact_budget=budget):
+            res = sg.global_align_packed(batch)
         for k, (t, p) in enumerate(zip(texts, pats)):
             d, cig, score = O.global_align(t, p)
             assert (int(res.distance[k]), res.cigar_string(k)) == (d, cig), (k, len(t), len(p))
