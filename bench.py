@@ -279,14 +279,23 @@ def main_reference(args):
 # BASELINE.md §4): name, generator id, W, O, pairs, the CPU reference's rate per
 # core for sizing its bounded sample, description.
 CONFIGS = [
-    ("cfg1", 1, 64, 24, 10_000, 17000, "short plumbing: 110/100 bp, 5% edits 1:1:1"),
-    ("cfg2", 2, 64, 24, 1_000_000, 9600, "Illumina-like: 250 bp reads, 2% edits 8:1:1"),
-    ("cfg4_W32_O12", 4, 32, 12, 20_000, 240, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
-    ("cfg4_W64_O24", 4, 64, 24, 20_000, 182, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
-    ("cfg4_W64_O33", 4, 64, 33, 20_000, 166, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
-    ("cfg4_W128_O48", 4, 128, 48, 20_000, 110, "W/O sweep: 10 kbp, 10% edits 1:1:1"),
-    ("cfg5", 5, 64, 24, 500_000, 300, "mixed 100..20k bp (log-uniform), 30% unrelated"),
+    ("cfg1", 1, 64, 24, 10_000, 17000, "short plumbing: 110/100 bp, 5% edits 1:1:1", (1, 1, 1)),
+    ("cfg2", 2, 64, 24, 1_000_000, 9600, "Illumina-like: 250 bp reads, 2% edits 8:1:1", (1, 1, 1)),
+    ("cfg4_W32_O12", 4, 32, 12, 20_000, 240, "W/O sweep: 10 kbp, 10% edits 1:1:1", (1, 1, 1)),
+    ("cfg4_W64_O24", 4, 64, 24, 20_000, 182, "W/O sweep: 10 kbp, 10% edits 1:1:1", (1, 1, 1)),
+    ("cfg4_W64_O33", 4, 64, 33, 20_000, 166, "W/O sweep: 10 kbp, 10% edits 1:1:1", (1, 1, 1)),
+    ("cfg4_W128_O48", 4, 128, 48, 20_000, 110, "W/O sweep: 10 kbp, 10% edits 1:1:1", (1, 1, 1)),
+    # the early-termination ablation (proj/src/dp.cpp:177, acceptance.cpp:160-194):
+    # the same pairs with ET off compute all W + 1 rows of every window
+    ("cfg4_W64_O24_et_off", 4, 64, 24, 20_000, 57, "W/O sweep: 10 kbp, 10% edits 1:1:1",
+     (1, 1, 0)),
+    ("cfg5", 5, 64, 24, 500_000, 300, "mixed 100..20k bp (log-uniform), 30% unrelated", (1, 1, 1)),
 ]
+
+
+def digest_name(name, cfg_id, W_, O_, switches):
+    s_, d_, e_ = switches
+    return f"cfg4_W{W_}_O{O_}_s{s_}d{d_}e{e_}" if cfg_id == 4 else f"cfg{cfg_id}"
 
 
 def digest_parity(res, name):
@@ -340,8 +349,9 @@ def measure_config(sg, name, cfg_id, W_, O_, pairs, rate_per_core, desc, steps, 
     cells = int(res.total.cells_computed)
     alg_ops = 4 * ((W_ + 31) // 32) * cells
     k1_s = sum(k1) / len(k1) / 1e3
-    parity = digest_parity(res, name)
+    parity = digest_parity(res, digest_name(name, cfg_id, W_, O_, switches))
     launches = int(res.gpu_launches)
+    rows = int(res.total.rows_computed)
     del res
     sg.align_packed(cfg, batch)  # warm the one-shot path
     t0 = time.perf_counter()
@@ -362,6 +372,7 @@ def measure_config(sg, name, cfg_id, W_, O_, pairs, rate_per_core, desc, steps, 
                      "peak": round(peak_ops / 1e12, 3), "unit": "Tops/s (int32 lane-ops)",
                      "frac": round(alg_ops / k1_s / peak_ops, 4), "alg_ops_per_launch": alg_ops,
                      "k1_ms": round(1e3 * k1_s, 3)},
+        "reference_counters": {"rows_computed": rows, "cells_computed": cells},
         "gpu_launches_per_step": launches,
         "parity": parity,
         "gen_seconds": round(t_gen, 2),
@@ -509,10 +520,10 @@ def main_ours(args):
     if rank == 0 and n_gpus == 1 and not args.headline_only:
         del batches, e2e_batch
         per_config = {}
-        for (name, cid, w_, o_, n_, rate, desc) in CONFIGS:
+        for (name, cid, w_, o_, n_, rate, desc, sw) in CONFIGS:
             per_config[name] = measure_config(sg, name, cid, w_, o_, n_, rate, desc,
                                               args.config_steps, args.warmup, peak,
-                                              not args.no_cpu_baseline)
+                                              not args.no_cpu_baseline, sw)
 
     if rank == 0:
         line = {

@@ -24,10 +24,15 @@
  *                            errors.hpp:10-34
  *
  * Semantics: identical edit distance and CIGAR to the reference for every
- * pair at the same (W, O, sene, dent, early_termination). The switches only
- * change work and footprint in the reference (proj/tests/acceptance.cpp:93-126);
- * the GPU always runs early termination with a 2-bit-per-cell trimmed table
- * and reports the reference's counters for the requested switches.
+ * pair at the same (W, O, sene, dent, early_termination). The switches change
+ * work and footprint in the reference, not results (proj/tests/acceptance.cpp:
+ * 93-126). On the GPU early_termination changes the work the same way: with it
+ * a window stops at the first row d with D(0, 0) <= d (dp.cpp:177, in chunks of
+ * 4 rows); without it every kernel computes all K + 1 rows of every window
+ * (dp.cpp:225; such batches run the full-frame K1 or K6). sene / dent select the
+ * reference's storage policy, whose counters are reported; the device itself
+ * always keeps 2-bit traceback events for the columns the traceback can reach
+ * (DENT's region), never the reference's table.
  */
 #ifndef SCROOGE_B200_H
 #define SCROOGE_B200_H

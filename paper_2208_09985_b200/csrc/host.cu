@@ -234,6 +234,14 @@ struct DevState {
     // diagnostics (SG_DIAG_*) of the last launch on this device
     DevBuf diag_warp, diag_phase;
     int diag_warps = 0, diag_flags = 0;
+    // sliced output (one-shot calls, §5): K2/K3 per slice of finished pairs on their
+    // own stream while K1 runs, each slice's run bytes copied out as soon as it is ready
+    static constexpr int kMaxSlices = 32;
+    DevBuf slice_done;
+    cudaStream_t slice_stream = nullptr, d2h = nullptr;
+    cudaEvent_t slice_go = nullptr, slices_done = nullptr, ev_slice[kMaxSlices] = {};
+    int64_t* slice_info = nullptr;  // host-mapped [2 * kMaxSlices]: (first byte, bytes)
+    int64_t runs_estimate = 0;      // run bytes of the last sliced call (staging size)
 
     void init(int dev) {
         device = dev;
@@ -243,6 +251,14 @@ struct DevState {
         SG_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
         SG_CUDA_CHECK(cudaEventCreateWithFlags(&copy_go, cudaEventDisableTiming));
         SG_CUDA_CHECK(cudaEventCreateWithFlags(&copy_done, cudaEventDisableTiming));
+        SG_CUDA_CHECK(cudaStreamCreateWithFlags(&slice_stream, cudaStreamNonBlocking));
+        SG_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        SG_CUDA_CHECK(cudaEventCreateWithFlags(&slice_go, cudaEventDisableTiming));
+        SG_CUDA_CHECK(cudaEventCreateWithFlags(&slices_done, cudaEventDisableTiming));
+        for (auto& e : ev_slice) SG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        void* info = nullptr;
+        SG_CUDA_CHECK(cudaHostAlloc(&info, 16 * kMaxSlices, cudaHostAllocMapped | cudaHostAllocPortable));
+        slice_info = static_cast<int64_t*>(info);
         for (auto& e : ev) SG_CUDA_CHECK(cudaEventCreate(&e));
     }
     ~DevState() {
@@ -253,8 +269,15 @@ struct DevState {
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
                           &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state,
-                          &u_list, &diag_warp, &diag_phase})
+                          &u_list, &diag_warp, &diag_phase, &slice_done})
             b->release();
+        if (slice_stream) cudaStreamDestroy(slice_stream);
+        if (d2h) cudaStreamDestroy(d2h);
+        if (slice_go) cudaEventDestroy(slice_go);
+        if (slices_done) cudaEventDestroy(slices_done);
+        for (auto& e : ev_slice)
+            if (e) cudaEventDestroy(e);
+        if (slice_info) cudaFreeHost(slice_info);
         if (copy) cudaStreamDestroy(copy);
         if (copy_go) cudaEventDestroy(copy_go);
         if (copy_done) cudaEventDestroy(copy_done);
@@ -434,13 +457,19 @@ struct ResultOwner {
     PinBuf distance, windows, found, cigar_off, runs, counters;
 };
 
-void results_alloc(sg_results* out, int64_t n, int64_t run_bytes) {
+// `staged`: a pinned buffer that already holds the run bytes (the sliced D2H);
+// the result takes it over instead of allocating its own.
+void results_alloc(sg_results* out, int64_t n, int64_t run_bytes, PinBuf* staged = nullptr) {
     auto own = std::make_unique<ResultOwner>();
     const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
     own->distance.ensure(8 * n1);
     own->windows.ensure(4 * n1);
     own->found.ensure(n1);
     own->cigar_off.ensure(8 * (n1 + 1));
+    if (staged && staged->p) {
+        std::swap(own->runs.p, staged->p);
+        std::swap(own->runs.cap, staged->cap);
+    }
     own->runs.ensure(static_cast<size_t>(std::max<int64_t>(run_bytes, 1)));
     own->counters.ensure(8 * SG_CNT_COUNT * n1);
     std::memset(out, 0, sizeof *out);
@@ -647,7 +676,11 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
     r.O = c->O;
     r.et = c->early_termination ? 1 : 0;
     r.policy = c->dent ? 2 : c->sene ? 1 : 0;
-    r.band = !r.wide && sgk::band_eligible(r.W, r.O, r.single) && kernel != SG_KERNEL_FULL;
+    // The mixed kernel always stops a window at D(0, 0) (its band frame is exact only
+    // up to row 30). Without early termination every window computes all K + 1 rows,
+    // as compute_dc does (proj/src/dp.cpp:177,225): the full-frame K1 and K6 do.
+    r.band = !r.wide && sgk::band_eligible(r.W, r.O, r.single) && kernel != SG_KERNEL_FULL &&
+             c->early_termination;
     return r;
 }
 
@@ -775,7 +808,10 @@ int64_t pairs_in_flight(const DevState& st, const RunConfig& rc, int64_t n) {
 }
 
 // Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
-int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
+// slices > 0 (one-shot calls): K2/K3 run per slice of `slice_pairs` pairs on the
+// slice stream while K1 runs; ev_slice[s] marks slice s's bytes dense on the device.
+int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int slices = 0,
+                 int32_t slice_pairs = 0) {
     const int64_t n = pp.n;
     const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
     st.distance.ensure(4 * n1);
@@ -863,6 +899,14 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
         p.phase_cycles = st.diag_phase.as<unsigned long long>();
     }
 
+    if (slices > 0) {
+        st.slice_done.ensure(4 * DevState::kMaxSlices);
+        SG_CUDA_CHECK(cudaMemsetAsync(st.slice_done.p, 0, 4 * DevState::kMaxSlices, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.dense_off.p, 0, 8, st.stream));
+        p.slice_done = st.slice_done.as<unsigned int>();
+        p.slice_pairs = slice_pairs;
+        SG_CUDA_CHECK(cudaEventRecord(st.slice_go, st.stream));
+    }
     int launches = 0;
     SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
     if (n > 0 && rc.band) {
@@ -910,6 +954,27 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
     SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
     // trailing pieces of a streamed upload no pair waited for finish before the call does
     SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.copy_done, 0));
+    if (slices > 0) {
+        SG_CUDA_CHECK(cudaStreamWaitEvent(st.slice_stream, st.slice_go, 0));
+        for (int sl = 0; sl < slices; ++sl) {
+            const int32_t lo = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl} * slice_pairs));
+            const int32_t hi = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl + 1} * slice_pairs));
+            int64_t* info = nullptr;
+            SG_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&info), st.slice_info, 0));
+            SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_slice_scan(
+                st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), lo, hi,
+                st.slice_done.as<unsigned>(), sl, info, st.slice_stream)));
+            SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_slice_compact(
+                st.scratch.as<uint32_t>(), st.bound_off.as<int64_t>(), st.dense_off.as<int64_t>(),
+                st.out_bytes.as<int32_t>(), st.dense.as<uint8_t>(), lo, hi, st.slice_stream)));
+            SG_CUDA_CHECK(cudaEventRecord(st.ev_slice[sl], st.slice_stream));
+            launches += hi > lo ? 2 : 1;
+        }
+        SG_CUDA_CHECK(cudaEventRecord(st.slices_done, st.slice_stream));
+        SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.slices_done, 0));
+        SG_CUDA_CHECK(cudaEventRecord(st.ev[2], st.stream));
+        return launches;
+    }
     SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_cigar_offsets(
         st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), static_cast<int32_t>(n),
         st.scan_tmp.p, st.scan_tmp.cap, st.stream)));
@@ -925,6 +990,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp) {
 // Small per-pair outputs of a shard, staged in pinned memory.
 struct ShardOut {
     PinBuf dist, win, status, doff, cnt;
+    PinBuf runs;          // sliced calls: the run bytes, already copied out
+    bool staged = false;
     int64_t run_bytes = 0;
     float device_ms = 0, k1_ms = 0;
     int launches = 0;
@@ -967,6 +1034,39 @@ void fetch_small(DevState& st, int64_t n, ShardOut& so) {
     SG_CUDA_CHECK(cudaEventElapsedTime(&k1, st.ev[0], st.ev[1]));
     so.device_ms = ms;
     so.k1_ms = k1;
+}
+
+// The sliced D2H (§5): slice by slice, as soon as K2/K3 have made its bytes dense,
+// the run bytes go to a pinned staging buffer on the d2h stream, overlapping K1.
+// The buffer is sized from the last call (grown, rarely, when a batch needs more);
+// the result takes it over.
+void stream_runs(DevState& st, int slices, int64_t bound_total, ShardOut& o) {
+    int64_t want = st.runs_estimate > 0 ? st.runs_estimate + st.runs_estimate / 8 + (int64_t{1} << 20)
+                                        : std::max<int64_t>(int64_t{64} << 20, bound_total / 4);
+    want = std::max<int64_t>(1, std::min(want, bound_total));
+    o.runs.ensure(static_cast<size_t>(want));
+    int64_t end = 0;
+    for (int sl = 0; sl < slices; ++sl) {
+        SG_CUDA_CHECK(cudaEventSynchronize(st.ev_slice[sl]));
+        const volatile int64_t* info = st.slice_info;
+        const int64_t base = info[2 * sl], bytes = info[2 * sl + 1];
+        if (base + bytes > static_cast<int64_t>(o.runs.cap)) {
+            SG_CUDA_CHECK(cudaStreamSynchronize(st.d2h));
+            PinBuf bigger;
+            bigger.ensure(static_cast<size_t>(std::max(bound_total, base + bytes)));
+            if (base) std::memcpy(bigger.p, o.runs.p, static_cast<size_t>(base));
+            std::swap(bigger.p, o.runs.p);
+            std::swap(bigger.cap, o.runs.cap);
+        }
+        if (bytes)
+            SG_CUDA_CHECK(cudaMemcpyAsync(o.runs.as<uint8_t>() + base, st.dense.as<uint8_t>() + base,
+                                          static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, st.d2h));
+        end = base + bytes;
+    }
+    SG_CUDA_CHECK(cudaStreamSynchronize(st.d2h));
+    st.runs_estimate = end;
+    o.staged = true;
+    o.d2h_bytes += end;
 }
 
 const char* status_detail(int32_t s) {
@@ -1205,8 +1305,18 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "plan", since_ms(t0));
 
     bool mixed = false;
-    for (int64_t k = 1; k < n && !mixed; ++k)
-        mixed = in->text_len[k] + in->pat_len[k] != in->text_len[0] + in->pat_len[0];
+    int64_t lmin = INT64_MAX, lmax = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t l = in->text_len[k] + in->pat_len[k];
+        lmin = std::min(lmin, l);
+        lmax = std::max(lmax, l);
+    }
+    mixed = n > 1 && lmax != lmin;
+    // One device: the run bytes leave in slices while K1 still runs (§5). Slices are
+    // ranges of input order, so near-equal pairs (cfg2/3/4) go in input order rather
+    // than longest first: slices then finish roughly one after another.
+    const bool sliced = nd == 1 && n >= 4096;
+    const bool uniform = 4 * lmax <= 5 * lmin;
 
     std::vector<ShardOut> so(nd);
     std::vector<ShardPrep> prep(nd);
@@ -1256,7 +1366,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             run_total += so[d].run_bytes;
         }
         try {
-            results_alloc(out, n, run_total);
+            results_alloc(out, n, run_total, nd == 1 && so[0].staged ? &so[0].runs : nullptr);
         } catch (const Fail& f) {
             fail_code = f.code;
             fail_msg = g_last_error;
@@ -1321,10 +1431,22 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             RunConfig rcs = rcfg;
             rcs.band = rcfg.band && band_pays(s.in, s.lo, s.hi, rcfg.W, rcfg.O);
             const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
-            prep_shard(s, prep[d], mixed, split);
+            prep_shard(s, prep[d], mixed && !(sliced && uniform), split);
             o.h2d_bytes += upload_shard(st, s, prep[d], streamed, true);
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "upload", since_ms(t0));
-            o.launches = launch_shard(st, rcs, prep[d]);
+            const int64_t sn = s.hi - s.lo;
+            int slices = 0;
+            int32_t per = 0;
+            if (sliced) {
+                slices = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices, std::max<int64_t>(1, sn / 4096)));
+                per = static_cast<int32_t>((sn + slices - 1) / slices);
+                slices = static_cast<int>((sn + per - 1) / per);
+            }
+            o.launches = launch_shard(st, rcs, prep[d], slices, per);
+            if (slices) {
+                stream_runs(st, slices, prep[d].scratch_bytes, o);
+                if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "runs d2h", since_ms(t0));
+            }
             fetch_small(st, prep[d].n, o);
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "kernels", since_ms(t0));
         });
@@ -1354,6 +1476,8 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
                     std::memcpy(out->counters + g * SG_CNT_COUNT, cnt + k * SG_CNT_COUNT,
                                 8 * SG_CNT_COUNT);
                 }
+            } else if (o.staged) {  // run bytes already in the result (sliced D2H)
+                scatter_small(out, plan.cut[d], plan.cut[d + 1] - plan.cut[d], run_base[d], o);
             } else {
                 if (o.run_bytes)
                     SG_CUDA_CHECK(cudaMemcpyAsync(out->runs + run_base[d], st.dense.p,
@@ -1362,7 +1486,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
                 scatter_small(out, plan.cut[d], plan.cut[d + 1] - plan.cut[d], run_base[d], o);
                 SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
             }
-            o.d2h_bytes += o.run_bytes;
+            if (!o.staged) o.d2h_bytes += o.run_bytes;
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "results", since_ms(t0));
         });
     };

@@ -691,6 +691,10 @@ __global__ void __launch_bounds__(32 * kWarps) k6_wide_align(const AlignParams P
                 c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
                 c[6] = c_bequiv;
             }
+            if (P.slice_done) {
+                __threadfence();
+                atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
+            }
         }
         __syncwarp();
     }

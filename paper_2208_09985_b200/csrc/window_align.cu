@@ -1218,6 +1218,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
             c[6] = c_bequiv;
         }
+        if (P.slice_done) {  // the pair's outputs are visible before its slice counts it
+            __threadfence();
+            atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
+        }
         if (P.mixed) atomicSub(P.remaining, 1u);
     };
 
@@ -1987,6 +1991,10 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                     for (int k = 0; k < 7; ++k) c[k] = cn[k];
                     c[5] = static_cast<unsigned long long>(nwin) * static_cast<unsigned>(K + 1);
                 }
+                if (P.slice_done) {
+                    __threadfence();
+                    atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
+                }
                 atomicSub(P.remaining, 1u);
             } else {
                 P.distance[pair] = dist;
@@ -2180,7 +2188,71 @@ __global__ void k3_compact(const uint32_t* __restrict__ scratch, const int64_t* 
     }
 }
 
+constexpr int kSliceBlock = 256;  // small: co-resident with K1's persistent blocks
+
+__global__ void __launch_bounds__(kSliceBlock)
+    k2_slice_scan(const int32_t* __restrict__ bytes, int64_t* __restrict__ dense_off, int32_t lo,
+                  int32_t hi, const unsigned* __restrict__ slice_done, int s, int64_t* info) {
+    __shared__ long long warp_tot[kSliceBlock / 32];
+    __shared__ long long carry;
+    if (threadIdx.x == 0) {
+        const unsigned want = static_cast<unsigned>(hi - lo);
+        while (*reinterpret_cast<const volatile unsigned*>(slice_done + s) < want) __nanosleep(2000);
+        __threadfence();
+        carry = lo == 0 ? 0 : dense_off[lo];
+    }
+    __syncthreads();
+    const long long base0 = carry;
+    for (int b0 = lo; b0 < hi; b0 += kSliceBlock) {
+        const int idx = b0 + threadIdx.x;
+        const long long v = idx < hi ? __ldcg(bytes + idx) : 0;
+        const long long inc = warp_incl_scan(v);
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        if (lane == 31) warp_tot[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const long long t = warp_incl_scan(lane < kSliceBlock / 32 ? warp_tot[lane] : 0);
+            if (lane < kSliceBlock / 32) warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const long long wbase = w > 0 ? warp_tot[w - 1] : 0;
+        if (idx < hi) dense_off[idx] = carry + wbase + inc - v;
+        __syncthreads();
+        if (threadIdx.x == kSliceBlock - 1) carry += wbase + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        dense_off[hi] = carry;
+        volatile int64_t* vi = info;
+        vi[2 * s] = base0;
+        vi[2 * s + 1] = carry - base0;
+        __threadfence_system();
+    }
+}
+
 }  // namespace
+
+int launch_slice_scan(const int32_t* out_bytes, int64_t* dense_off, int32_t lo, int32_t hi,
+                      const unsigned* slice_done, int s, int64_t* info, void* stream) {
+    k2_slice_scan<<<1, kSliceBlock, 0, static_cast<cudaStream_t>(stream)>>>(out_bytes, dense_off, lo,
+                                                                          hi, slice_done, s, info);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_slice_compact(const uint32_t* scratch, const int64_t* bound_off, const int64_t* dense_off,
+                         const int32_t* out_bytes, uint8_t* dense, int32_t lo, int32_t hi,
+                         void* stream) {
+    if (hi <= lo) return 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int threads = 128;
+    long long blocks = (static_cast<long long>(hi - lo) * 32 + threads - 1) / threads;
+    if (blocks > 2ll * sms) blocks = 2ll * sms;
+    k3_compact<<<static_cast<int>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        scratch, bound_off + lo, dense_off + lo, out_bytes + lo, dense, hi - lo);
+    return static_cast<int>(cudaGetLastError());
+}
 
 int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_block, void* stream) {
     (void)warps_per_block;

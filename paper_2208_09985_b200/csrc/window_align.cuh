@@ -87,6 +87,10 @@ struct AlignParams {
     int32_t* resume_state;    // [n_pairs][4]: toff, poff, cur_op | cur_len << 8, open word
     int32_t* u_list;          // K0 (§3.10): unrelated pairs, left to a full-frame K1 launch
     unsigned int* u_count;
+    // finished-pair counts per output slice (one-shot calls): a pair's run bytes and
+    // counts are complete when its slice's count includes it (null: no slices)
+    unsigned int* slice_done;
+    int32_t slice_pairs;      // pairs per slice (pair k is in slice k / slice_pairs)
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
@@ -160,5 +164,15 @@ size_t cigar_offsets_temp_bytes(int32_t n);
 int launch_cigar_compact(const uint32_t* scratch, const int64_t* bound_off,
                          const int64_t* dense_off, const int32_t* out_bytes, uint8_t* dense,
                          int32_t n, void* stream);
+// K2/K3 per output slice [lo, hi) while K1 still runs (one-shot calls, on a second
+// stream): waits until the slice's pairs have all finished (slice_done[s] == hi - lo),
+// scans their run byte counts onto the running offset (dense_off[lo] holds the
+// previous slices' total; dense_off[hi] receives the new one), compacts their bytes,
+// and reports (first byte, bytes) of the slice in info[2s], info[2s + 1] (host-mapped).
+int launch_slice_scan(const int32_t* out_bytes, int64_t* dense_off, int32_t lo, int32_t hi,
+                      const unsigned* slice_done, int s, int64_t* info, void* stream);
+int launch_slice_compact(const uint32_t* scratch, const int64_t* bound_off,
+                         const int64_t* dense_off, const int32_t* out_bytes, uint8_t* dense,
+                         int32_t lo, int32_t hi, void* stream);
 
 }  // namespace sgk
