@@ -539,10 +539,11 @@ constexpr int kBackRow = SG_BACK_ROW;  // a pair goes back to the band warps aft
 constexpr int kCoopSleep = SG_COOP_SLEEP;  // ns between an idle cooperative warp's polls
 // per-warp shared memory, in 32-bit words:
 //   eqp [WMAX + 4][32] uint2  (EQ_i, parked row) of column i at slot i + 4
-//   xy  [CMAX + 1][32] uint2  events X / Y; column C (runtime) is the dummy
+//   xy  [CMAX + 2][32] uint2  parity planes (P0, P1) of columns 0..C; column C + 1
+//                             (runtime) is the dummy
 //   sq  packed text / pattern / N words of the window (traceback), as K1<2>
 __host__ __device__ constexpr int eqp_words() { return (WMAX + 4) * 64; }
-__host__ __device__ constexpr int xy_words() { return (CMAX + 1) * 64; }
+__host__ __device__ constexpr int xy_words() { return (CMAX + 2) * 64; }
 }  // namespace band
 
 struct BandState {
@@ -550,7 +551,7 @@ struct BandState {
     uint32_t dg[4];      // row r-1's value at row r's column + 1 (row 0: parked row)
     uint32_t dgs[4];     // dg << 1
     uint32_t eq[4];      // EQ ring: slot s & 3 = the column row 0 entered at step s
-    uint32_t acc[4][2];  // X / Y ring, same slots
+    uint32_t acc[4][2];  // parity planes (P0, P1) ring, same slots
 };
 
 __device__ __forceinline__ uint32_t fma_shl(uint32_t x, uint32_t two) {  // x * two (IMAD)
@@ -578,13 +579,17 @@ __device__ __forceinline__ void band_cell(BandState& S, uint32_t north, uint32_t
     const uint32_t mt = STD ? es : east;  // the match neighbour (i+1, j+1)
     const uint32_t dl = STD ? east : es;  // the deletion neighbour (i+1, j)
     const uint32_t c = (mt & S.eq[SL]) | S.dg[r] | S.dgs[r] | ns;
+    (void)dl;
     if (CAP) {
-        if (r == 0) {
-            S.acc[SL][0] = mt & ~c;
-            S.acc[SL][1] = dl & ~c;
-        } else {
-            S.acc[SL][0] |= mt & ~c;
-            S.acc[SL][1] |= dl & ~c;
+        // parity planes of the column (§3.8): P0 ^= every row, P1 ^= the odd rows
+        // (d0 is a multiple of 4, so row r's parity is r's). Row 1 takes rows 0 and
+        // 1 (north = row 0 at this column), row 3 rows 2 and 3.
+        if (r == 1) {
+            S.acc[SL][0] = north ^ c;
+            S.acc[SL][1] = c;
+        } else if (r == 3) {
+            S.acc[SL][0] ^= north ^ c;
+            S.acc[SL][1] ^= c;
         }
     }
     if (r + 1 < 4) {
@@ -608,7 +613,7 @@ struct BandMem {
 // finished column keeps events), kBMix (stores of columns >= C go to the dummy).
 template <int MODE, int U, bool STD>
 __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const BandMem& M,
-                                          int col_top, int C, uint32_t keep, uint32_t two,
+                                          int col_top, int C, uint32_t two,
                                           uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
                                           uint32_t one_l, bool live) {
     constexpr bool CAP = MODE != kBOut;
@@ -641,14 +646,10 @@ __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const Ban
         // another frame's parked row)
         if (live) reinterpret_cast<uint32_t*>(M.eqp + (c3 + 4) * 32)[1] = S.v[3];
         if (STORE_EV) {
-            // (old & keep) | acc as old * keep + acc on the FMA pipe: an event bit
-            // is set by at most one row of a window (X: D(i+1,j+1) <= d < D(i,j)
-            // and D(i,j) - D(i+1,j+1) <= 1; Y likewise), so old and acc are disjoint
+            // the planes of a window start at zero (load_segment) and XOR over its
+            // chunks; an idle lane's all-zero rows leave them unchanged
             constexpr int SL3 = (U + 1) & 3;
-            uint2 o;
-            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(o.x) : "r"(old.x), "r"(keep), "r"(S.acc[SL3][0]));
-            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(o.y) : "r"(old.y), "r"(keep), "r"(S.acc[SL3][1]));
-            *px = o;
+            *px = make_uint2(old.x ^ S.acc[SL3][0], old.y ^ S.acc[SL3][1]);
         }
     }
 }
@@ -659,13 +660,13 @@ __device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const Ban
 // finished column keeps events), kBMix (stores of columns >= C go to the dummy).
 template <int MODE, bool STD>
 __device__ __forceinline__ void band_group(BandState& S, uint2 (&F)[4], const BandMem& M,
-                                           int col_top, int C, uint32_t keep, uint32_t two,
+                                           int col_top, int C, uint32_t two,
                                            uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
                                            uint32_t one_l, bool live) {
-    band_step<MODE, 0, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 1, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 2, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 3, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 0, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 1, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 2, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_step<MODE, 3, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
 }
 
 // init column (i = n_w) of row d: bits k in [K0 - d, K0] (D(n, j) = m - j <= d)
@@ -682,9 +683,6 @@ template <bool STD>
 __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K0, int k00,
                                           const BandMem& M, uint32_t two, uint32_t hmul) {
     const uint32_t lv = live ? ~0u : 0u;
-    // a live lane's first chunk of a window overwrites the events; otherwise adds
-    // (as a multiplier: 0 or 1)
-    const uint32_t keep = live && d0 == 0 ? 0u : 1u;
     BandState S;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -698,17 +696,17 @@ __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K
     uint2 F[4];
 #pragma unroll
     for (int U = 0; U < 4; ++U) F[U] = M.eqp[(W - 1 - U + 4) * 32];
-    band_group<kBFill, STD>(S, F, M, W - 1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+    band_group<kBFill, STD>(S, F, M, W - 1, C, two, hmul, two_l, hmul_l, one_l, live);
     // steady groups in three runs (no per-group mode test): right of the event
     // columns, the one or two groups that straddle column C, inside them
     int col_top = W - 5;
     for (; col_top >= 3 && col_top - 3 >= C; col_top -= 4)
-        band_group<kBOut, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+        band_group<kBOut, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
     for (; col_top >= 3 && col_top + 3 >= C; col_top -= 4)
-        band_group<kBMix, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+        band_group<kBMix, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
     for (; col_top >= 3; col_top -= 4)
-        band_group<kBIn, STD>(S, F, M, col_top, C, keep, two, hmul, two_l, hmul_l, one_l, live);
-    band_group<kBDrain, STD>(S, F, M, -1, C, keep, two, hmul, two_l, hmul_l, one_l, live);
+        band_group<kBIn, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_group<kBDrain, STD>(S, F, M, -1, C, two, hmul, two_l, hmul_l, one_l, live);
     int fr = -1;
 #pragma unroll
     for (int r = 3; r >= 0; --r)
@@ -995,6 +993,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     bmem.eqp[(16 * k + u + 4) * 32] = make_uint2(e, 0u);
                 }
             }
+            for (int c = 0; c <= cmax; ++c) bmem.xy[c * 32] = make_uint2(0u, 0u);  // planes start at 0
 #pragma unroll
             for (int k = 0; k <= L; ++k) {
                 sq_tn[k * 32 + lane] = tn[k];
@@ -1057,6 +1056,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, i & 31), 0u);
                 }
             }
+            // the parity planes of the window start at zero (the LUT above is dead)
+            for (int c = 0; c <= cmax; ++c) bmem.xy[c * 32] = make_uint2(0u, 0u);
 #pragma unroll
             for (int k = 0; k <= L; ++k) {
                 sq_tn[k * 32 + lane] = tn[k];
@@ -1393,11 +1394,11 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 const bool act_b = act && !std_win, act_s = act && std_win;
                 int fr = -1;
                 if (__any_sync(kFull, act_b)) {
-                    const int f = band_chunk<false>(act_b, d0, W, cmax, K0, -e_lo, bmem, two, hmul);
+                    const int f = band_chunk<false>(act_b, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
                     if (act_b) fr = f;
                 }
                 if (__any_sync(kFull, act_s)) {
-                    const int f = band_chunk<true>(act_s, d0, W, cmax, m_w, 0, bmem, two, hmul);
+                    const int f = band_chunk<true>(act_s, d0, W, cmax + 1, m_w, 0, bmem, two, hmul);
                     if (act_s) fr = f;
                 }
                 ++ph_it;
@@ -1421,6 +1422,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             }
             int fr = -1;
             if (!BAND && bnd_smem) {  // mixed full-frame warp: STD windows first
+                // (compiled out: its traceback reads X / Y events, band_chunk writes planes)
+                static_assert(band::FWARPS == 0, "band_chunk writes parity planes");
                 const bool act_std = act && std_win;
                 if (__any_sync(kFull, act_std)) {
                     const int f = band_chunk<true>(act_std, d0, W, C, m_w, 0, bmem, two, hmul);
@@ -1532,24 +1535,37 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 }
                 if (k != run || run == 16 || rem == 0 || i == n_w || j == m_w || i >= cmax) continue;
                 // the edit at the mismatch (i, j)
-                const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
-                uint32_t bit;
-                if (BAND && std_win) {
-                    bit = 1u << j;
-                } else if constexpr (BAND) {  // diagonal band: cell (i, j) at bit j - i - e_lo
-                    const int kb = j - i - e_lo;
-                    if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
-                        status = kStInternal | kDetSegment;
-                        break;
+                int op;
+                if constexpr (BAND) {
+                    // parity planes of column i + 1 (§3.8): a cell with n = #(rows
+                    // 0..dm holding it) has D = dm + 1 - n; P0 = n & 1, P1 = #(odd
+                    // rows holding it) & 1. The two neighbours of a path cell are
+                    // within 1 of d, so D(nbr) == d - 1 <=> (P0, P1) == (E0, E1).
+                    const uint2 pl = *reinterpret_cast<const uint2*>(xy + (i + 1) * 64 + lane * 2);
+                    const int dm = d0 + R - 1;  // the window's last computed row
+                    const uint32_t e0 = static_cast<uint32_t>(dm - d) & 1u;
+                    const uint32_t e1 = static_cast<uint32_t>(((dm + 1) >> 1) - ((d - 1) >> 1)) & 1u;
+                    const uint32_t lt = (pl.x ^ (e0 - 1u)) & (pl.y ^ (e1 - 1u));  // D(nbr) == d - 1
+                    int kb;  // the bit of (i + 1, j + 1); (i + 1, j) is the one below
+                    if (std_win) {
+                        kb = j + 1;
+                    } else {  // diagonal band: cell (i, j) at bit j - i - e_lo
+                        kb = j - i - e_lo;
+                        if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
+                            status = kStInternal | kDetSegment;
+                            break;
+                        }
                     }
-                    bit = 1u << kb;
+                    op = (lt >> kb) & 1u ? 1 : (((lt << 1) >> kb) & 1u ? 3 : 2);
                 } else {
+                    const uint2 ev = *reinterpret_cast<const uint2*>(xy + i * 64 + lane * 2);
+                    uint32_t bit;
                     const unsigned q = static_cast<unsigned>(j + off);
                     const int dp = static_cast<int>(q / L) - band_base<L>(i, off);
                     if (!std_win && static_cast<unsigned>(dp) >= 32u / L) break;  // left the band
                     bit = std_win ? 1u << j : 0x80000000u >> ((32 / L) * (q % L) + dp);
+                    op = ev.x & bit ? 1 : (ev.y & bit ? 3 : 2);
                 }
-                const int op = ev.x & bit ? 1 : (ev.y & bit ? 3 : 2);
                 if (d == 0) status = kStInternal | kDetNoStep;
                 reads += d == 0 ? 1u : 3u;
                 i += op != 2;
