@@ -941,6 +941,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
         pu.u_list = nullptr;
         pu.order = st.u_list.as<int32_t>();
         pu.n_fresh = reinterpret_cast<const int32_t*>(p.u_count);
+        pu.restore = 1;  // unrelated pairs from their start, the others from their tail
         pu.next_pair = st.next_pair.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_window_align(rc.L, pu, static_cast<int>(grid), wpb, st.stream)));

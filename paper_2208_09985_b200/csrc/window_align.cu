@@ -26,8 +26,11 @@ template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2, MINB
 #ifndef SG_SUBCHUNKS
 #define SG_SUBCHUNKS 2
 #endif
+#ifndef SG_BAND_R
+#define SG_BAND_R 8  // rows per band chunk (kBandR)
+#endif
 #ifndef SG_BAND_SUBCHUNKS
-#define SG_BAND_SUBCHUNKS 4
+#define SG_BAND_SUBCHUNKS (16 / SG_BAND_R)  // 16 rows per phase
 #endif
 constexpr int kSubChunks = SG_SUBCHUNKS;
 constexpr int kBandSubChunks = SG_BAND_SUBCHUNKS;
@@ -528,7 +531,10 @@ constexpr int CMAX = 40;              // traceback-event columns (W - O <= 40)
 constexpr int kLastRow = 30;          // rows 0..30 are exact
 constexpr int WARPS = 7;              // band warps per block (one block per SM) ...
 constexpr int FWARPS = 0;             // (no full-frame warp in K1 mixed) ...
-constexpr int CWARPS = 2;             // ... plus cooperative warps
+#ifndef SG_CWARPS
+#define SG_CWARPS 1
+#endif
+constexpr int CWARPS = SG_CWARPS;             // ... plus cooperative warps
 #ifndef SG_BACK_ROW
 #define SG_BACK_ROW 24
 #endif
@@ -546,12 +552,17 @@ __host__ __device__ constexpr int eqp_words() { return (WMAX + 4) * 64; }
 __host__ __device__ constexpr int xy_words() { return (CMAX + 2) * 64; }
 }  // namespace band
 
+// Band chunks are R = 8 rows (kBandR): eight independent cells per step, and the
+// per-column work (EQ / parked-row load, park, plane update) spread over 8 cells.
+constexpr int kBandR = SG_BAND_R;
+
+template <int R>
 struct BandState {
-    uint32_t v[4];       // row r's latest value
-    uint32_t dg[4];      // row r-1's value at row r's column + 1 (row 0: parked row)
-    uint32_t dgs[4];     // dg << 1
-    uint32_t eq[4];      // EQ ring: slot s & 3 = the column row 0 entered at step s
-    uint32_t acc[4][2];  // parity planes (P0, P1) ring, same slots
+    uint32_t v[R];       // row r's latest value
+    uint32_t dg[R];      // row r-1's value at row r's column + 1 (row 0: parked row)
+    uint32_t dgs[R];     // dg << 1
+    uint32_t eq[R];      // EQ ring: slot s % R = the column row 0 entered at step s
+    uint32_t acc[R][2];  // parity planes (P0, P1) ring, same slots
 };
 
 __device__ __forceinline__ uint32_t fma_shl(uint32_t x, uint32_t two) {  // x * two (IMAD)
@@ -564,37 +575,43 @@ __device__ __forceinline__ uint32_t fma_shr(uint32_t x, uint32_t hmul) {  // x *
     asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(hmul));
     return r;
 }
+// (a & b) | c | d as two LOP3s (ptxas otherwise often emits three)
+__device__ __forceinline__ uint32_t or_and4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t e) {
+    uint32_t t, r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(t) : "r"(a), "r"(b), "r"(c));  // (a & b) | c
+    asm("lop3.b32 %0, %1, %2, %3, 0xFE;" : "=r"(r) : "r"(t), "r"(d), "r"(e));  // t | d | e
+    return r;
+}
 
 // Row r's cell at step U (static). north: row r-1's value at this column.
 // STD: the standard frame (bit j = cell (i, j), patterns of <= 31 bases, §3.8):
 //   C[i][d] = ((C[i+1][d] >> 1) & EQ_i) | (C[i+1][d-1] >> 1) | C[i+1][d-1] | (C[i][d-1] >> 1)
-// X = (C[i+1][d] >> 1) & ~C, Y = C[i+1][d] & ~C; the same data flow with es = east >> 1.
-template <int U, int r, bool CAP, bool STD>
-__device__ __forceinline__ void band_cell(BandState& S, uint32_t north, uint32_t two,
+// the band chunk's data flow with es = east >> 1.
+template <int R, int U, int r, bool CAP, bool STD>
+__device__ __forceinline__ void band_cell(BandState<R>& S, uint32_t north, uint32_t two,
                                           uint32_t hmul) {
-    constexpr int SL = (U - r) & 3;
+    constexpr int SL = (U - r) & (R - 1);
     const uint32_t east = S.v[r];
     const uint32_t ns = fma_shr(north, hmul);
     const uint32_t es = STD ? fma_shr(east, hmul) : fma_shl(east, two);
     const uint32_t mt = STD ? es : east;  // the match neighbour (i+1, j+1)
-    const uint32_t dl = STD ? east : es;  // the deletion neighbour (i+1, j)
-    const uint32_t c = (mt & S.eq[SL]) | S.dg[r] | S.dgs[r] | ns;
-    (void)dl;
+    const uint32_t c = or_and4(mt, S.eq[SL], S.dg[r], S.dgs[r], ns);
     if (CAP) {
         // parity planes of the column (§3.8): P0 ^= every row, P1 ^= the odd rows
-        // (d0 is a multiple of 4, so row r's parity is r's). Row 1 takes rows 0 and
-        // 1 (north = row 0 at this column), row 3 rows 2 and 3.
+        // (d0 is a multiple of R, so row r's parity is r's). An odd row r takes
+        // rows r - 1 and r into P0 (north = row r - 1 at this column).
         if (r == 1) {
             S.acc[SL][0] = north ^ c;
             S.acc[SL][1] = c;
-        } else if (r == 3) {
+        } else if (r & 1) {
             S.acc[SL][0] ^= north ^ c;
             S.acc[SL][1] ^= c;
         }
     }
-    if (r + 1 < 4) {
-        S.dg[r + 1 < 4 ? r + 1 : 0] = east;
-        S.dgs[r + 1 < 4 ? r + 1 : 0] = es;
+    if (r + 1 < R) {
+        S.dg[r + 1 < R ? r + 1 : 0] = east;
+        S.dgs[r + 1 < R ? r + 1 : 0] = es;
     }
     S.v[r] = c;
 }
@@ -607,66 +624,66 @@ struct BandMem {
     uint2* xy;   // column c at xy[c * 32]
 };
 
-// One group of 4 steps. Row 0 works on columns col_top .. col_top - 3; row r
-// lags r columns. MODE: kBFill (rows r <= U start at column W-1), kBDrain
-// (rows r > U finish at column 0), kBOut (no event columns), kBIn (every
-// finished column keeps events), kBMix (stores of columns >= C go to the dummy).
-template <int MODE, int U, bool STD>
-__device__ __forceinline__ void band_step(BandState& S, uint2 (&F)[4], const BandMem& M,
+template <int R, int MODE, int U, bool STD, int r>
+__device__ __forceinline__ void band_rows(BandState<R>& S, uint32_t two, uint32_t hmul) {
+    // rows R-1..1, descending: a row reads its upper row's value before it updates
+    if constexpr (r >= 1) {
+        if constexpr ((MODE == kBFill && r <= U) || (MODE == kBDrain && r > U) ||
+                      (MODE != kBFill && MODE != kBDrain))
+            band_cell<R, U, r, MODE != kBOut, STD>(S, S.v[r - 1], two, hmul);
+        band_rows<R, MODE, U, STD, r - 1>(S, two, hmul);
+    }
+}
+
+// Step U of a group of R steps. Row 0 works on columns col_top .. col_top - R + 1;
+// row r lags r columns. MODE: kBFill (rows r <= U start at column W-1), kBDrain
+// (rows r > U finish at column 0), kBOut (no plane columns), kBIn (every column
+// the last row finishes keeps its planes), kBMix (stores of columns >= C go to the
+// dummy). F: (EQ, parked row) of row 0's column, loaded four steps ahead.
+template <int R, int MODE, int U, bool STD>
+__device__ __forceinline__ void band_step(BandState<R>& S, uint2 (&F)[4], const BandMem& M,
                                           int col_top, int C, uint32_t two,
                                           uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
                                           uint32_t one_l, bool live) {
     constexpr bool CAP = MODE != kBOut;
-    constexpr bool ROW3 = (MODE == kBFill ? U == 3 : true) && (MODE != kBDrain || U < 3);
-    constexpr bool STORE_EV = CAP && ROW3;
-    const int c3 = col_top - U + 3;  // the column row 3 finishes at this step
-    uint2* px = M.xy + (MODE == kBIn ? c3 : (c3 < C ? c3 : C)) * 32;
+    constexpr bool LAST = (MODE == kBFill ? U == R - 1 : true) && (MODE != kBDrain || U < R - 1);
+    constexpr bool STORE_EV = CAP && LAST;
+    const int cl = col_top - U + R - 1;  // the column the last row finishes at this step
+    uint2* px = M.xy + (MODE == kBIn ? cl : (cl < C ? cl : C)) * 32;
     uint2 old = make_uint2(0u, 0u);
     if (STORE_EV) old = *px;
-    const uint2 f = F[U];
-    // rows 3..1 (descending: a row reads its upper row's value before it updates)
-#define SG_BCELL(r)                                                                   \
-    if ((MODE == kBFill && (r) <= U) || (MODE == kBDrain && (r) > U) ||               \
-        (MODE != kBFill && MODE != kBDrain))                                          \
-        band_cell<U, (r), CAP, STD>(S, S.v[(r) - 1], two, hmul);
-    SG_BCELL(3) SG_BCELL(2) SG_BCELL(1)
-#undef SG_BCELL
+    const uint2 f = F[U & 3];
+    band_rows<R, MODE, U, STD, R - 1>(S, two, hmul);
     if (MODE != kBDrain) {  // row 0: north = parked row of this column, masked for idle lanes
         S.eq[U] = f.x;
-        band_cell<U, 0, CAP, STD>(S, f.y, two, hmul_l);
-        // (right of the event columns the FMA pipe is the busier one: AND there)
+        band_cell<R, U, 0, CAP, STD>(S, f.y, two, hmul_l);
+        // (right of the plane columns the FMA pipe is the busier one: AND there)
         S.dg[0] = MODE == kBOut ? f.y & (0u - one_l) : fma_shl(f.y, one_l);
         S.dgs[0] = STD ? fma_shr(f.y, hmul_l) : fma_shl(f.y, two_l);
-        // next group's column, into the registers f just left (no copies at the
-        // end of the group); used four steps on
-        F[U] = M.eqp[(col_top - U - 4 + 4) * 32];
+        // row 0's column four steps on, into the registers f just left
+        F[U & 3] = M.eqp[(col_top - U - 4 + 4) * 32];
     }
-    if (ROW3) {
-        // park row 3 (idle lanes do not: in a full-frame warp the slot may be
-        // another frame's parked row)
-        if (live) reinterpret_cast<uint32_t*>(M.eqp + (c3 + 4) * 32)[1] = S.v[3];
+    if (LAST) {
+        // park the last row (idle lanes do not)
+        if (live) reinterpret_cast<uint32_t*>(M.eqp + (cl + 4) * 32)[1] = S.v[R - 1];
         if (STORE_EV) {
             // the planes of a window start at zero (load_segment) and XOR over its
             // chunks; an idle lane's all-zero rows leave them unchanged
-            constexpr int SL3 = (U + 1) & 3;
-            *px = make_uint2(old.x ^ S.acc[SL3][0], old.y ^ S.acc[SL3][1]);
+            constexpr int SLL = (U + 1) & (R - 1);
+            *px = make_uint2(old.x ^ S.acc[SLL][0], old.y ^ S.acc[SLL][1]);
         }
     }
 }
 
-// One group of 4 steps. Row 0 works on columns col_top .. col_top - 3; row r
-// lags r columns. MODE: kBFill (rows r <= U start at column W-1), kBDrain
-// (rows r > U finish at column 0), kBOut (no event columns), kBIn (every
-// finished column keeps events), kBMix (stores of columns >= C go to the dummy).
-template <int MODE, bool STD>
-__device__ __forceinline__ void band_group(BandState& S, uint2 (&F)[4], const BandMem& M,
+template <int R, int MODE, bool STD, int U = 0>
+__device__ __forceinline__ void band_group(BandState<R>& S, uint2 (&F)[4], const BandMem& M,
                                            int col_top, int C, uint32_t two,
                                            uint32_t hmul, uint32_t two_l, uint32_t hmul_l,
                                            uint32_t one_l, bool live) {
-    band_step<MODE, 0, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 1, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 2, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    band_step<MODE, 3, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    if constexpr (U < R) {
+        band_step<R, MODE, U, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+        band_group<R, MODE, STD, U + 1>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    }
 }
 
 // init column (i = n_w) of row d: bits k in [K0 - d, K0] (D(n, j) = m - j <= d)
@@ -676,16 +693,16 @@ __device__ __forceinline__ uint32_t band_init(int d, int K0) {
     return (0xFFFFFFFFu >> (31 - K0)) & (0xFFFFFFFFu << lo);
 }
 
-// One chunk of rows d0..d0+3 over the W columns of a band window. Returns the
-// first row r with D(0, 0) <= d0 + r, or -1. Idle lanes (live = false) run on
-// all-zero rows: they keep their stored events and park zeros.
-template <bool STD>
+// One chunk of rows d0..d0+R-1 over the W columns (W % R == 0) of a band window.
+// Returns the first row r with D(0, 0) <= d0 + r, or -1. Idle lanes (live = false)
+// run on all-zero rows: they keep their stored planes and do not park.
+template <int R, bool STD>
 __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K0, int k00,
                                           const BandMem& M, uint32_t two, uint32_t hmul) {
     const uint32_t lv = live ? ~0u : 0u;
-    BandState S;
+    BandState<R> S;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < R; ++r) {
         S.v[r] = band_init(d0 + r, K0) & lv;
         S.dg[r] = band_init(d0 + r - 1, K0) & lv;
         S.dgs[r] = STD ? S.dg[r] >> 1 : S.dg[r] << 1;
@@ -696,20 +713,20 @@ __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K
     uint2 F[4];
 #pragma unroll
     for (int U = 0; U < 4; ++U) F[U] = M.eqp[(W - 1 - U + 4) * 32];
-    band_group<kBFill, STD>(S, F, M, W - 1, C, two, hmul, two_l, hmul_l, one_l, live);
-    // steady groups in three runs (no per-group mode test): right of the event
-    // columns, the one or two groups that straddle column C, inside them
-    int col_top = W - 5;
-    for (; col_top >= 3 && col_top - 3 >= C; col_top -= 4)
-        band_group<kBOut, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    for (; col_top >= 3 && col_top + 3 >= C; col_top -= 4)
-        band_group<kBMix, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    for (; col_top >= 3; col_top -= 4)
-        band_group<kBIn, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
-    band_group<kBDrain, STD>(S, F, M, -1, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_group<R, kBFill, STD>(S, F, M, W - 1, C, two, hmul, two_l, hmul_l, one_l, live);
+    // steady groups in three runs (no per-group mode test): right of the plane
+    // columns, the groups that straddle column C, inside them
+    int col_top = W - 1 - R;
+    for (; col_top >= R - 1 && col_top - (R - 1) >= C; col_top -= R)
+        band_group<R, kBOut, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    for (; col_top >= R - 1 && col_top + R - 1 >= C; col_top -= R)
+        band_group<R, kBMix, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    for (; col_top >= R - 1; col_top -= R)
+        band_group<R, kBIn, STD>(S, F, M, col_top, C, two, hmul, two_l, hmul_l, one_l, live);
+    band_group<R, kBDrain, STD>(S, F, M, -1, C, two, hmul, two_l, hmul_l, one_l, live);
     int fr = -1;
 #pragma unroll
-    for (int r = 3; r >= 0; --r)
+    for (int r = R - 1; r >= 0; --r)
         if ((S.v[r] >> k00) & 1u) fr = r;
     return fr;
 }
@@ -1138,15 +1155,11 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 // a window the STD frame takes never runs in the band frame: STD is
                 // exact for every row (a band failure would otherwise come back here)
                 if (!band_ok || std_ok) {
-                    // STD windows stay in this lane once no fresh pairs are left (the
-                    // end of the batch: full-frame warps alone would drain them slowly)
-                    if (std_ok && *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
-                                      static_cast<unsigned>(n_fresh)) {
-                        std_win = true;
-                    } else {
-                        hand_to = std_ok ? 3 : 2;  // STD queue (band warps drain it at the end) or cooperative
-                        return 2;
-                    }
+                    // the pair's tail (a final window, or a window of a pattern or text
+                    // with fewer than W bases left) goes to the full-frame K1 after
+                    // this kernel; a full window (mid-pair) to a cooperative warp
+                    hand_to = fin || n_w < W || m_w < W || !P.u_list ? 3 : 2;
+                    return 2;
                 } else {
                     e_lo = (dl >> 1) - 16;
                     K0 = dl - e_lo;
@@ -1171,15 +1184,6 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 
     // Hand the pair to the next pass (the other frame) before its current window.
     auto defer_pair = [&]() {
-        if (BAND && hand_to == 2 && nwin == 0 && P.u_list) {
-            // K0 (§3.10): the pair's first window already has D(0, 0) > 30 (an
-            // unrelated pair: every window would go to a cooperative warp) or is
-            // not band-shaped at all. The full-frame K1 after this kernel aligns
-            // it from the start.
-            P.u_list[atomicAdd(P.u_count, 1u)] = pair;
-            atomicSub(P.remaining, 1u);
-            return;
-        }
         P.distance[pair] = dist;
         P.windows[pair] = nwin;
         P.status[pair] = 0;
@@ -1198,6 +1202,15 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         rs[1] = poff;
         rs[2] = (cur_op & 0xFF) | (cur_len << 8);
         rs[3] = static_cast<int32_t>(acc);
+        if (BAND && P.u_list && (hand_to == 3 || (hand_to == 2 && (nwin == 0 || m_w < W)))) {
+            // the full-frame K1 after this kernel resumes the pair from its state: its
+            // tail (§3.10), or all of it (K0: the first window already has D(0, 0) >
+            // 30, an unrelated pair whose every window would go to a cooperative
+            // warp, or is not band-shaped at all)
+            P.u_list[atomicAdd(P.u_count, 1u)] = pair;
+            atomicSub(P.remaining, 1u);
+            return;
+        }
         q_push(hand_to == 0 ? P.q_band : hand_to == 1 ? P.q_full : hand_to == 2 ? P.q_coop : P.q_std,
                P.n_pairs, pair);
     };
@@ -1252,6 +1265,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 base = __shfl_sync(wm, base, leader);
                 const int q = static_cast<int>(base + __popc(wm & ((1u << lane) - 1u)));
                 pair = q < n_fresh ? (P.order ? P.order[q] : q) : -1;
+                restore = P.restore != 0;
                 if (P.warp_times && pair < 0 && ph_fresh_end == 0)  // diagnostics
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ph_fresh_end));
             }
@@ -1394,29 +1408,29 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 const bool act_b = act && !std_win, act_s = act && std_win;
                 int fr = -1;
                 if (__any_sync(kFull, act_b)) {
-                    const int f = band_chunk<false>(act_b, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
+                    const int f = band_chunk<kBandR, false>(act_b, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
                     if (act_b) fr = f;
                 }
                 if (__any_sync(kFull, act_s)) {
-                    const int f = band_chunk<true>(act_s, d0, W, cmax + 1, m_w, 0, bmem, two, hmul);
+                    const int f = band_chunk<kBandR, true>(act_s, d0, W, cmax + 1, m_w, 0, bmem, two, hmul);
                     if (act_s) fr = f;
                 }
                 ++ph_it;
                 ph_act += __popc(__ballot_sync(kFull, act));
                 if (act && std_win) {  // the STD frame is exact for every row
                     if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
-                    solved = found_d >= 0 || d0 + R > K;
-                    if (!solved) d0 += R;
+                    solved = found_d >= 0 || d0 + kBandR > K;
+                    if (!solved) d0 += kBandR;
                 } else if (act) {
                     if (found_d < 0 && fr >= 0) found_d = d0 + fr;
                     // D(0, 0) is exact up to band_last; beyond it the window goes
                     // to a cooperative warp
-                    solved = found_d >= 0 || d0 + R > band_last;
+                    solved = found_d >= 0 || d0 + kBandR > band_last;
                     if (solved && (found_d < 0 || found_d > band_last)) {
                         defer_now = true;
                         hand_to = 2;
                     }
-                    if (!solved) d0 += R;
+                    if (!solved) d0 += kBandR;
                 }
                 continue;
             }
@@ -1426,7 +1440,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 static_assert(band::FWARPS == 0, "band_chunk writes parity planes");
                 const bool act_std = act && std_win;
                 if (__any_sync(kFull, act_std)) {
-                    const int f = band_chunk<true>(act_std, d0, W, C, m_w, 0, bmem, two, hmul);
+                    const int f = band_chunk<4, true>(act_std, d0, W, C, m_w, 0, bmem, two, hmul);
                     if (act_std) fr = f;
                     ++ph_it;
                     ph_act += __popc(__ballot_sync(kFull, act_std));
@@ -1542,7 +1556,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     // rows holding it) & 1. The two neighbours of a path cell are
                     // within 1 of d, so D(nbr) == d - 1 <=> (P0, P1) == (E0, E1).
                     const uint2 pl = *reinterpret_cast<const uint2*>(xy + (i + 1) * 64 + lane * 2);
-                    const int dm = d0 + R - 1;  // the window's last computed row
+                    const int dm = d0 + kBandR - 1;  // the window's last computed row
                     const uint32_t e0 = static_cast<uint32_t>(dm - d) & 1u;
                     const uint32_t e1 = static_cast<uint32_t>(((dm + 1) >> 1) - ((d - 1) >> 1)) & 1u;
                     const uint32_t lt = (pl.x ^ (e0 - 1u)) & (pl.y ^ (e1 - 1u));  // D(nbr) == d - 1
@@ -2313,7 +2327,7 @@ int mixed_max_blocks_per_sm(int LF) {
 }
 
 bool band_eligible(int W, int O, int single) {
-    return !single && W >= 4 && W <= band::WMAX && W % 4 == 0 && W - O >= 1 &&
+    return !single && W >= kBandR && W <= band::WMAX && W % kBandR == 0 && W - O >= 1 &&
            W - O <= band::CMAX;
 }
 

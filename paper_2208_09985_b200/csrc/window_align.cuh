@@ -85,8 +85,9 @@ struct AlignParams {
     uint32_t* q_std;          // pairs whose next window the STD frame takes (m_w <= 31)
     unsigned int* remaining;  // pairs not finished (warps exit at 0)
     int32_t* resume_state;    // [n_pairs][4]: toff, poff, cur_op | cur_len << 8, open word
-    int32_t* u_list;          // K0 (§3.10): unrelated pairs, left to a full-frame K1 launch
-    unsigned int* u_count;
+    int32_t* u_list;          // K0 (§3.10): pairs left to a full-frame K1 launch after the
+    unsigned int* u_count;    // mixed one (unrelated pairs and every pair's tail windows)
+    int32_t restore;          // the fresh pairs resume from resume_state (that launch)
     // finished-pair counts per output slice (one-shot calls): a pair's run bytes and
     // counts are complete when its slice's count includes it (null: no slices)
     unsigned int* slice_done;
