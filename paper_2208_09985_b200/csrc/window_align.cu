@@ -982,7 +982,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             load_bits<L + 1>(P.nmask, pbase + poff, pn);
             load_bits<L + 1>(P.nmask, tbase + toff, tn);
         }
-        if (std_win) {
+        if (!BAND && std_win) {
             // (§3.8) STD frame: EQ_i = plane t_i of the pattern, bits j < m_w <= 31;
             // the planes go to this lane's event columns 0..3 (dead until the first
             // chunk overwrites them), the parked row starts as row -1 (zeros)
@@ -1405,23 +1405,11 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             const bool act = in_dc && !solved;
             if (sub > 0 && !__any_sync(kFull, act)) break;
             if constexpr (BAND) {
-                const bool act_b = act && !std_win, act_s = act && std_win;
-                int fr = -1;
-                if (__any_sync(kFull, act_b)) {
-                    const int f = band_chunk<kBandR, false>(act_b, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
-                    if (act_b) fr = f;
-                }
-                if (__any_sync(kFull, act_s)) {
-                    const int f = band_chunk<kBandR, true>(act_s, d0, W, cmax + 1, m_w, 0, bmem, two, hmul);
-                    if (act_s) fr = f;
-                }
+                // (band warps never hold an STD window: those are pair tails, §3.10)
+                int fr = band_chunk<kBandR, false>(act, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
                 ++ph_it;
                 ph_act += __popc(__ballot_sync(kFull, act));
-                if (act && std_win) {  // the STD frame is exact for every row
-                    if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
-                    solved = found_d >= 0 || d0 + kBandR > K;
-                    if (!solved) d0 += kBandR;
-                } else if (act) {
+                if (act) {
                     if (found_d < 0 && fr >= 0) found_d = d0 + fr;
                     // D(0, 0) is exact up to band_last; beyond it the window goes
                     // to a cooperative warp
