@@ -930,7 +930,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
             st.stream)));
         // K0 (§3.10): band warps leave unrelated pairs to a full-frame K1 after them
         st.u_list.ensure(4 * n1);
-        SG_CUDA_CHECK(cudaMemsetAsync(st.mixed_ctr.as<unsigned int>() + 8, 0, 4, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.mixed_ctr.as<unsigned int>() + 8, 0, 8, st.stream));
+        p.coop_out = st.mixed_ctr.as<unsigned int>() + 9;
         p.u_list = st.u_list.as<int32_t>();
         p.u_count = st.mixed_ctr.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(

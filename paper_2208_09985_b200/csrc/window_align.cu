@@ -1158,7 +1158,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     // the pair's tail (a final window, or a window of a pattern or text
                     // with fewer than W bases left) goes to the full-frame K1 after
                     // this kernel; a full window (mid-pair) to a cooperative warp
-                    hand_to = fin || n_w < W || m_w < W || !P.u_list ? 3 : 2;
+                    hand_to = (fin || n_w < W || m_w < W) && P.u_list ? 3 : 2;
                     return 2;
                 } else {
                     e_lo = (dl >> 1) - 16;
@@ -1211,6 +1211,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             atomicSub(P.remaining, 1u);
             return;
         }
+        if (BAND && hand_to == 2) atomicAdd(P.coop_out, 1u);  // before the pair is visible
         q_push(hand_to == 0 ? P.q_band : hand_to == 1 ? P.q_full : hand_to == 2 ? P.q_coop : P.q_std,
                P.n_pairs, pair);
     };
@@ -1243,13 +1244,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     auto fetch = [&]() {
         pair = -1;
         bool restore = false;
-        if (P.mixed) {  // a pair handed over by the other frame first
-            pair = q_pop_warp(BAND ? P.q_band : P.q_full, P.n_pairs, true);
-            const bool fresh_left = BAND && *reinterpret_cast<const volatile unsigned*>(P.next_pair) <
-                                                static_cast<unsigned>(n_fresh);
-            // band warps take STD windows once no fresh pairs are left
-            const int sp = q_pop_warp(P.q_std, P.n_pairs, pair < 0 && !fresh_left);
-            if (pair < 0) pair = sp;
+        if (P.mixed) {  // a pair handed back by a cooperative warp first (if any is out)
+            const bool back = !BAND || *reinterpret_cast<const volatile unsigned*>(P.coop_out) != 0u;
+            pair = q_pop_warp(BAND ? P.q_band : P.q_full, P.n_pairs, back);
+            if (BAND && pair >= 0) atomicSub(P.coop_out, 1u);
             restore = pair >= 0;
         }
         if (BAND || !P.mixed) {  // fresh pairs (warp-aggregated claim)
@@ -1386,6 +1384,12 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         const bool in_dc = pair >= 0;
         if (!__any_sync(kFull, in_dc)) {
             if (!P.mixed || *reinterpret_cast<const volatile unsigned*>(P.remaining) == 0u) break;
+            // a band warp with nothing left to take: no fresh pair, none out at a
+            // cooperative warp (the only way one can come back)
+            if (BAND && *reinterpret_cast<const volatile unsigned*>(P.next_pair) >=
+                            static_cast<unsigned>(n_fresh) &&
+                *reinterpret_cast<const volatile unsigned*>(P.coop_out) == 0u)
+                break;
 
             // pairs are still in flight: one may be handed to this warp
             idle_wait(BAND ? 4000 : 16000);
@@ -1710,7 +1714,6 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
             if (next_held == nheld) {
                 next_held = 0;
                 nheld = q_pop_n(P.q_coop, P.n_pairs, 8, held);
-                if (nheld == 0) nheld = q_pop_n(P.q_std, P.n_pairs, 8, held);
             }
             if (next_held < nheld) pair = held[next_held++];
         }
@@ -2014,6 +2017,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                     atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
                 }
                 atomicSub(P.remaining, 1u);
+                atomicSub(P.coop_out, 1u);
             } else {
                 P.distance[pair] = dist;
                 P.windows[pair] = nwin;

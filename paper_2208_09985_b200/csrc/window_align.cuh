@@ -88,6 +88,8 @@ struct AlignParams {
     int32_t* u_list;          // K0 (§3.10): pairs left to a full-frame K1 launch after the
     unsigned int* u_count;    // mixed one (unrelated pairs and every pair's tail windows)
     int32_t restore;          // the fresh pairs resume from resume_state (that launch)
+    unsigned int* coop_out;   // pairs a band warp handed to a cooperative warp and not yet
+                              // taken back (in q_coop, at a cooperative warp, or in q_band)
     // finished-pair counts per output slice (one-shot calls): a pair's run bytes and
     // counts are complete when its slice's count includes it (null: no slices)
     unsigned int* slice_done;
