@@ -735,7 +735,9 @@ __device__ __forceinline__ int band_chunk(bool live, int d0, int W, int C, int K
 
 // Shared memory words of one K1 warp (BAND: the band-frame layout, §3.8).
 template <int L, bool BAND> __host__ __device__ constexpr int k1_warp_words() {
-    return BAND ? band::eqp_words() + band::xy_words() + sq_words<L>() : warp_smem_words<L>();
+    // band: rings of 8 packed words per side plus the N words (sq_words<2> with PFW 8)
+    return BAND ? band::eqp_words() + band::xy_words() + (2 * 8 + 2 * (L + 1)) * 32
+                : warp_smem_words<L>();
 }
 // Hand-over queues between band and full-frame warps (K1 mixed, §3.8): a ring
 // of pair ids, q[0] = head, q[1] = tail, slots q[32 + k % cap] hold pair + 1
@@ -836,7 +838,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     // warps of the mixed kernel: STD windows use the parked-row region
     const BandMem bmem{reinterpret_cast<uint2*>(BAND ? wbase : eqp_smem) + lane,
                        reinterpret_cast<uint2*>(xy) + lane};
-    constexpr int PFW = pf_words<L>();
+    // band warps stage each side's packed words in a ring of 8 (the window needs 6;
+    // the next one starts <= 3 words on) refilled from 3 prefetched words
+    constexpr int PFW = BAND ? 8 : pf_words<L>();
+    constexpr int NXW = BAND ? 3 : PFW;
     uint32_t* const sq_t = sq;                                   // text staging (PFW words)
     uint32_t* const sq_p = sq + PFW * 32;                        // pattern staging (PFW)
     uint32_t* const sq_tn = sq + 2 * PFW * 32;                   // text N words (L+1)
@@ -887,9 +892,11 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     // the segment's text / pattern start at base t_sh / p_sh inside them. The
     // words of the region the next window can start in are prefetched into
     // registers (nx_t / nx_p) while the current window runs.
-    uint32_t nx_t[PFW], nx_p[PFW];
-    int64_t nx_tw = -1, nx_pw = -1;
+    uint32_t nx_t[NXW], nx_p[NXW];
+    int64_t nx_tw = -1, nx_pw = -1;  // band: one past the last staged word (-1: none)
+    int64_t pf_tw = -1, pf_pw = -1;  // band: first word in nx_t / nx_p
     int t_sh = 0, p_sh = 0;
+    int tb0 = 0, pb0 = 0;            // band: ring slot of the window's first word
     // output
     uint32_t* outw = nullptr;
     int out_bytes = 0, cur_op = -1, cur_len = 0, acc_n = 0;
@@ -936,7 +943,44 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         // upload a line read early into L1 could hold words of a chunk that had
         // not arrived yet (the staging reads run past the pair's end).
         uint32_t pw[NW + 1], pn[L + 1], tw[NW + 1], tn[L + 1];
-        {
+        if constexpr (BAND) {
+            const int64_t ta = tbase + toff, pa = pbase + poff;
+            const int64_t wt = ta >> 4, wp = pa >> 4;
+            auto stage = [&](uint32_t* ring, uint32_t (&nx)[NXW], int64_t& hi, int64_t& pf,
+                             int64_t w0) {
+                const int64_t need = w0 + 6;
+                if (hi < 0 || w0 < hi - 6 || need > hi + 3) {  // a new pair (or a jump)
+#pragma unroll
+                    for (int k = 0; k < 6; ++k)
+                        ring[((w0 + k) & 7) * 32 + lane] = __ldcg(P.seq + w0 + k);
+                    hi = need;
+                } else {
+                    const bool have = pf == hi;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        if (hi + k < need)
+                            ring[((hi + k) & 7) * 32 + lane] = have ? nx[k] : __ldcg(P.seq + hi + k);
+                    hi = max(hi, need);
+                }
+                // the words the next window can add (it starts <= 3 words on)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) nx[k] = __ldcg(P.seq + hi + k);
+                pf = hi;
+            };
+            stage(sq_t, nx_t, nx_tw, pf_tw, wt);
+            stage(sq_p, nx_p, nx_pw, pf_pw, wp);
+            t_sh = static_cast<int>(ta - 16 * wt);
+            p_sh = static_cast<int>(pa - 16 * wp);
+            tb0 = static_cast<int>(wt & 7);
+            pb0 = static_cast<int>(wp & 7);
+#pragma unroll
+            for (int k = 0; k <= NW; ++k) {
+                tw[k] = __funnelshift_r(sq_t[((tb0 + k) & 7) * 32 + lane],
+                                        sq_t[((tb0 + k + 1) & 7) * 32 + lane], 2 * t_sh);
+                pw[k] = __funnelshift_r(sq_p[((pb0 + k) & 7) * 32 + lane],
+                                        sq_p[((pb0 + k + 1) & 7) * 32 + lane], 2 * p_sh);
+            }
+        } else {
             const int64_t ta = tbase + toff, pa = pbase + poff;
             const int64_t wt = ta >> 4, wp = pa >> 4;
             // prefetched region usable? (it covers [16 nx_w, 16 (nx_w + PFW)))
@@ -1060,10 +1104,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (16 * k >= n_w) break;
-                const int bt = t_sh + 16 * k;
-                const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
-                                                       sq_t[((bt >> 4) + 1) * 32 + lane],
-                                                       2 * (bt & 15));
+                const uint32_t tword = tw[k];
                 const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
@@ -1320,9 +1361,12 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     // Matching bases from (i, j) on (0..16; 0 at a mismatch or a non-ACGT base).
     auto match_run = [&](int i, int j) -> int {
         const int bi = t_sh + i, bj = p_sh + j;
-        const int wi = bi >> 4, si = 2 * (bi & 15), wj = bj >> 4, sj = 2 * (bj & 15);
-        const uint32_t t0 = lds_v(sq_t + wi * 32 + lane), t1 = lds_v(sq_t + (wi + 1) * 32 + lane);
-        const uint32_t p0 = lds_v(sq_p + wj * 32 + lane), p1 = lds_v(sq_p + (wj + 1) * 32 + lane);
+        const int si = 2 * (bi & 15), sj = 2 * (bj & 15);
+        constexpr int RM = BAND ? 7 : 0xFFFF;  // band: ring slots
+        const int wi = (tb0 + (bi >> 4)) & RM, wi1 = (tb0 + (bi >> 4) + 1) & RM;
+        const int wj = (pb0 + (bj >> 4)) & RM, wj1 = (pb0 + (bj >> 4) + 1) & RM;
+        const uint32_t t0 = lds_v(sq_t + wi * 32 + lane), t1 = lds_v(sq_t + wi1 * 32 + lane);
+        const uint32_t p0 = lds_v(sq_p + wj * 32 + lane), p1 = lds_v(sq_p + wj1 * 32 + lane);
         uint32_t x = __funnelshift_r(t0, t1, si) ^ __funnelshift_r(p0, p1, sj);
         x = (x | (x >> 1)) & 0x55555555u;  // bit 2k: base k differs
         if (hasn) {
@@ -1524,6 +1568,48 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     cur_op = op;
                 }
             };
+            if constexpr (BAND) {
+                // band windows: n_w = W > lim = cmax, so the walk stops at the step
+                // limit or at the end of the pattern (m_w >= W - 30; the tail below
+                // takes the deletions left)
+                const int dm = d0 + kBandR - 1;  // the window's last computed row
+                int kb = -e_lo;                  // the bit of (i, j): j - i - e_lo
+                while (steps < lim && j < m_w) {
+                    ++ph_steps;
+                    ++tb_trip;
+                    const int run = match_run(i, j);
+                    const int k = min(run, min(lim - steps, m_w - j));
+                    reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
+                    i += k;
+                    j += k;
+                    steps += k;
+                    if (k > 0) emit_short(0, k);
+                    if (k != run || run == 16 || steps == lim || j == m_w) continue;
+                    // the edit at the mismatch (i, j), from the parity planes of column
+                    // i + 1 (§3.8): a cell held by n of rows 0..dm has D = dm + 1 - n;
+                    // P0 = n & 1, P1 = (odd rows holding it) & 1. The two neighbours of a
+                    // path cell are within 1 of d, so D(nbr) == d - 1 <=> (P0, P1) ==
+                    // (E0, E1). (i + 1, j + 1) is at bit kb, (i + 1, j) at kb - 1.
+                    if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
+                        status = kStInternal | kDetSegment;
+                        break;
+                    }
+                    const uint2 pl = *reinterpret_cast<const uint2*>(xy + (i + 1) * 64 + lane * 2);
+                    const uint32_t e0 = static_cast<uint32_t>(dm - d) & 1u;
+                    const uint32_t e1 = static_cast<uint32_t>(((dm + 1) >> 1) - ((d - 1) >> 1)) & 1u;
+                    const uint32_t lt = (pl.x ^ (e0 - 1u)) & (pl.y ^ (e1 - 1u));  // D(nbr) == d - 1
+                    const int op = (lt >> kb) & 1u ? 1 : (((lt << 1) >> kb) & 1u ? 3 : 2);
+                    if (d == 0) status = kStInternal | kDetNoStep;
+                    reads += d == 0 ? 1u : 3u;
+                    i += op != 2;
+                    j += op != 3;
+                    kb += (op == 2) - (op == 3);
+                    --d;
+                    ++dist;
+                    ++steps;
+                    emit_short(op, 1);
+                }
+            } else
             for (;;) {
                 ++ph_steps;
                 ++tb_trip;
