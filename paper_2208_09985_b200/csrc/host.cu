@@ -229,7 +229,7 @@ struct DevState {
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
     // K1 mixed (§3.8-3.10): hand-over queues, counters (remaining pairs, K0 count),
     // the handed pairs' state, K0's list of unrelated pairs
-    DevBuf q_band, q_full, q_coop, q_std, mixed_ctr, resume_state, u_list;
+    DevBuf q_band, q_full, q_coop, q_std, mixed_ctr, resume_state, u_list, t_list;
     long long grid = 0, lanes = 0;
     // diagnostics (SG_DIAG_*) of the last launch on this device
     DevBuf diag_warp, diag_phase;
@@ -268,7 +268,7 @@ struct DevState {
                           &distance, &windows, &status, &out_bytes, &counters, &bound_off,
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
-                          &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state,
+                          &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state, &t_list,
                           &u_list, &diag_warp, &diag_phase, &slice_done})
             b->release();
         if (slice_stream) cudaStreamDestroy(slice_stream);
@@ -930,12 +930,27 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
             st.stream)));
         // K0 (§3.10): band warps leave unrelated pairs to a full-frame K1 after them
         st.u_list.ensure(4 * n1);
-        SG_CUDA_CHECK(cudaMemsetAsync(st.mixed_ctr.as<unsigned int>() + 8, 0, 8, st.stream));
+        SG_CUDA_CHECK(cudaMemsetAsync(st.mixed_ctr.as<unsigned int>() + 8, 0, 12, st.stream));
         p.coop_out = st.mixed_ctr.as<unsigned int>() + 9;
+        st.t_list.ensure(4 * n1);
+        p.t_list = st.t_list.as<int32_t>();
+        p.t_count = st.mixed_ctr.as<unsigned int>() + 10;
         p.u_list = st.u_list.as<int32_t>();
         p.u_count = st.mixed_ctr.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
+        // the tail K1: the pairs' STD windows in the band warps' single-word frame
+        sgk::AlignParams pt = p;
+        pt.warp_times = nullptr;
+        pt.mixed = 0;
+        pt.t_list = nullptr;
+        pt.order = st.t_list.as<int32_t>();
+        pt.n_fresh = reinterpret_cast<const int32_t*>(p.t_count);
+        pt.next_pair = st.next_pair.as<unsigned int>() + 4;
+        pt.restore = 1;
+        pt.band_active = 0x7FFFFFFF;
+        SG_CUDA_CHECK(static_cast<cudaError_t>(
+            sgk::launch_tail_align(pt, static_cast<int>(st.sms), st.stream)));
         sgk::AlignParams pu = p;
         pu.warp_times = nullptr;
         pu.mixed = 0;
@@ -946,7 +961,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
         pu.next_pair = st.next_pair.as<unsigned int>() + 8;
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_window_align(rc.L, pu, static_cast<int>(grid), wpb, st.stream)));
-        launches += 3;
+        launches += 4;
     } else if (n > 0) {
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             rc.wide ? sgk::launch_wide_align(p, static_cast<int>(grid), st.stream)

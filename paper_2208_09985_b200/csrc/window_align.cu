@@ -1,6 +1,9 @@
 // K1 window_align (GenASM-DC + GenASM-TB + window loop) and K2/K3 CIGAR
 // offset scan / compaction, hand-written for sm_100a. Design: DESIGN.md §3.
 #include "window_align.cuh"
+#ifdef SG_DEBUG_POST
+#include <cstdio>
+#endif
 
 #include <cuda_runtime.h>
 
@@ -531,6 +534,9 @@ constexpr int CMAX = 40;              // traceback-event columns (W - O <= 40)
 constexpr int kLastRow = 30;          // rows 0..30 are exact
 constexpr int WARPS = 7;              // band warps per block (one block per SM) ...
 constexpr int FWARPS = 0;             // (no full-frame warp in K1 mixed) ...
+#ifndef SG_K0
+#define SG_K0 1  // a pair whose first window fails the band frame goes to the full-frame K1
+#endif
 #ifndef SG_CWARPS
 #define SG_CWARPS 1
 #endif
@@ -822,7 +828,7 @@ __device__ __forceinline__ int q_pop_warp(uint32_t* q, int cap, bool want) {
 // it cannot take (final windows, n_w < W, |m_w - n_w| > 30, D(0, 0) > 30) go
 // with the pair to a full-frame warp (P.mixed); a full-frame warp hands the
 // pair back once its next window is a band window again.
-template <int L, bool BAND>
+template <int L, bool BAND, bool TAIL = false>
 __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wbase,
                                         const long long gwarp, uint32_t* const bnd_smem,
                                         uint32_t* const eqp_smem) {
@@ -1026,7 +1032,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             load_bits<L + 1>(P.nmask, pbase + poff, pn);
             load_bits<L + 1>(P.nmask, tbase + toff, tn);
         }
-        if (!BAND && std_win) {
+        if ((!BAND || TAIL) && std_win) {
             // (§3.8) STD frame: EQ_i = plane t_i of the pattern, bits j < m_w <= 31;
             // the planes go to this lane's event columns 0..3 (dead until the first
             // chunk overwrites them), the parked row starts as row -1 (zeros)
@@ -1042,9 +1048,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             pl[3 * 64] = lo & hi & valid;
             for (int k = 0; 16 * k < n_w; ++k) {
                 const int bt = t_sh + 16 * k;
-                const uint32_t tword = __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
-                                                       sq_t[((bt >> 4) + 1) * 32 + lane],
-                                                       2 * (bt & 15));
+                const uint32_t tword = BAND ? tw[k]
+                                            : __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
+                                                              sq_t[((bt >> 4) + 1) * 32 + lane],
+                                                              2 * (bt & 15));
                 const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
@@ -1192,14 +1199,23 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             const bool wide_ok = !fin && n_w == W && m_w >= 32;
             const bool std_ok = !fin && n_w == W && m_w <= 31;  // the STD frame takes it
             std_win = false;
-            if (BAND) {
+            if (TAIL) {
+                // the tail K1 takes STD windows only; the rest of the pair goes on
+                // to the full-frame K1
+                if (!std_ok) {
+                    hand_to = 4;
+                    return 2;
+                }
+                std_win = true;
+            } else if (BAND) {
                 // a window the STD frame takes never runs in the band frame: STD is
                 // exact for every row (a band failure would otherwise come back here)
                 if (!band_ok || std_ok) {
-                    // the pair's tail (a final window, or a window of a pattern or text
-                    // with fewer than W bases left) goes to the full-frame K1 after
-                    // this kernel; a full window (mid-pair) to a cooperative warp
-                    hand_to = (fin || n_w < W || m_w < W) && P.u_list ? 3 : 2;
+                    // the pair's tail: an STD window (m_w <= 31) goes to the tail K1, a
+                    // final window to the full-frame K1 after it; any other window (|m_w
+                    // - n_w| > 30, a text or pattern all but consumed) to a cooperative
+                    // warp, which hands an STD window on to the tail K1
+                    hand_to = std_ok && P.t_list ? 5 : fin && P.u_list ? 4 : 2;
                     return 2;
                 } else {
                     e_lo = (dl >> 1) - 16;
@@ -1243,13 +1259,18 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         rs[1] = poff;
         rs[2] = (cur_op & 0xFF) | (cur_len << 8);
         rs[3] = static_cast<int32_t>(acc);
-        if (BAND && P.u_list && (hand_to == 3 || (hand_to == 2 && (nwin == 0 || m_w < W)))) {
+        if (BAND && hand_to == 5) {  // the tail K1 resumes the pair (its STD window)
+            P.t_list[atomicAdd(P.t_count, 1u)] = pair;
+            if (P.mixed) atomicSub(P.remaining, 1u);
+            return;
+        }
+        if (BAND && (hand_to == 4 || (SG_K0 && P.u_list && hand_to == 2 && nwin == 0))) {
             // the full-frame K1 after this kernel resumes the pair from its state: its
             // tail (§3.10), or all of it (K0: the first window already has D(0, 0) >
             // 30, an unrelated pair whose every window would go to a cooperative
             // warp, or is not band-shaped at all)
             P.u_list[atomicAdd(P.u_count, 1u)] = pair;
-            atomicSub(P.remaining, 1u);
+            if (P.mixed) atomicSub(P.remaining, 1u);
             return;
         }
         if (BAND && hand_to == 2) atomicAdd(P.coop_out, 1u);  // before the pair is visible
@@ -1257,7 +1278,19 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                P.n_pairs, pair);
     };
 
+#ifdef SG_DEBUG_POST
+    unsigned long long dbg_t0 = 0; int dbg_w0 = 0, dbg_t = 0, dbg_p = 0;
+#endif
     auto finish_pair = [&]() {
+#ifdef SG_DEBUG_POST
+        if (!BAND && P.restore) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - dbg_t0 > 100000ull)
+                printf("slow post pair %d: %llu ns, windows %d -> %d, n %d m %d, from toff %d poff %d dist %d status %x\n",
+                       pair, t - dbg_t0, dbg_w0, nwin, n_tot, m_tot, dbg_t, dbg_p, dist, status);
+        }
+#endif
         if (cur_op >= 0) put_byte((static_cast<uint32_t>(cur_op) << 6) | (cur_len - 1));
         if (acc_n) *outw = acc;
         P.distance[pair] = dist;
@@ -1333,6 +1366,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         acc_n = 0;
         c_stored = c_writes = c_reads = c_rows = c_cells = c_bequiv = 0;
         pass_win = 0;
+#ifdef SG_DEBUG_POST
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+#endif
         if (restore) {  // continue where the other frame stopped (state written before the push)
             const int4 rs = __ldcg(reinterpret_cast<const int4*>(P.resume_state + 4ll * pair));
             toff = rs.x;
@@ -1342,6 +1378,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             acc = static_cast<uint32_t>(rs.w);
             dist = __ldcg(P.distance + pair);
             nwin = __ldcg(P.windows + pair);
+#ifdef SG_DEBUG_POST
+            dbg_w0 = nwin; dbg_t = toff; dbg_p = poff;
+#endif
             out_bytes = __ldcg(P.out_bytes + pair);
             acc_n = out_bytes & 3;
             outw += out_bytes >> 2;
@@ -1453,11 +1492,17 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             const bool act = in_dc && !solved;
             if (sub > 0 && !__any_sync(kFull, act)) break;
             if constexpr (BAND) {
-                // (band warps never hold an STD window: those are pair tails, §3.10)
-                int fr = band_chunk<kBandR, false>(act, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
+                // (the main pass's band warps never hold an STD window: those are pair
+                // tails, run by the tail K1 in the STD frame, §3.10)
+                int fr = TAIL ? band_chunk<kBandR, true>(act, d0, W, cmax + 1, m_w, 0, bmem, two, hmul)
+                              : band_chunk<kBandR, false>(act, d0, W, cmax + 1, K0, -e_lo, bmem, two, hmul);
                 ++ph_it;
                 ph_act += __popc(__ballot_sync(kFull, act));
-                if (act) {
+                if (TAIL && act) {  // the STD frame is exact for every row
+                    if (found_d < 0 && fr >= 0 && d0 + fr <= K) found_d = d0 + fr;
+                    solved = found_d >= 0 || d0 + kBandR > K;
+                    if (!solved) d0 += kBandR;
+                } else if (act) {
                     if (found_d < 0 && fr >= 0) found_d = d0 + fr;
                     // D(0, 0) is exact up to band_last; beyond it the window goes
                     // to a cooperative warp
@@ -1573,7 +1618,8 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 // limit or at the end of the pattern (m_w >= W - 30; the tail below
                 // takes the deletions left)
                 const int dm = d0 + kBandR - 1;  // the window's last computed row
-                int kb = -e_lo;                  // the bit of (i, j): j - i - e_lo
+                // the bit of (i + 1, j + 1): band j - i - e_lo, STD (tail K1) j + 1
+                int kb = TAIL ? 1 : -e_lo;
                 while (steps < lim && j < m_w) {
                     ++ph_steps;
                     ++tb_trip;
@@ -1590,6 +1636,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     // P0 = n & 1, P1 = (odd rows holding it) & 1. The two neighbours of a
                     // path cell are within 1 of d, so D(nbr) == d - 1 <=> (P0, P1) ==
                     // (E0, E1). (i + 1, j + 1) is at bit kb, (i + 1, j) at kb - 1.
+                    if (TAIL) kb = j + 1;  // (the STD frame: bit j + 1)
                     if (static_cast<unsigned>(kb) >= 32u) {  // cannot happen for d <= 30
                         status = kStInternal | kDetSegment;
                         break;
@@ -1871,6 +1918,8 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
             const int n_w = min(W, n_rem), m_w = min(W, m_rem), dl = m_w - n_w;
             const bool band_ok = !fin && n_w == W && dl <= band::kLastRow && dl >= -band::kLastRow;
             if (pass_win > 0 && band_ok && last_d <= band::kBackRow) { hand = 0; break; }
+            // an STD window (m_w <= 31): the pair's tail, for the tail K1 (§3.10)
+            if (P.t_list && !fin && n_w == W && m_w <= 31) { hand = 5; break; }
             // this warp takes every other window: final ones (traceback to the
             // end, events of every column) and the tails of the STD queue too
             const int lim = fin ? 0x3FFFFFFF : step_limit, cap = fin ? n_w : step_limit;
@@ -2119,7 +2168,13 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                 r[1] = poff;
                 r[2] = (cur_op & 0xFF) | (cur_len << 8);
                 r[3] = static_cast<int32_t>(acc);
-                q_push(hand == 0 ? P.q_band : hand == 1 ? P.q_full : P.q_std, P.n_pairs, pair);
+                if (hand == 5) {
+                    P.t_list[atomicAdd(P.t_count, 1u)] = pair;
+                    atomicSub(P.remaining, 1u);
+                    atomicSub(P.coop_out, 1u);
+                } else {
+                    q_push(hand == 0 ? P.q_band : hand == 1 ? P.q_full : P.q_std, P.n_pairs, pair);
+                }
             }
         }
         __syncwarp();
@@ -2174,6 +2229,15 @@ __global__ void __launch_bounds__(32 * kMixedWarps, 1)
                            base + warp_smem_words<LF>(),
                            base + warp_smem_words<LF>() + mixed_eqp_offset<LF>());
     }
+}
+
+// The tail K1 (§3.10): the band warps alone (no cooperative warp), running the STD
+// windows of the pairs the mixed kernel left in its tail list.
+__global__ void __launch_bounds__(32 * band::WARPS, 1) k1_tail(const __grid_constant__ AlignParams P) {
+    extern __shared__ uint32_t smem[];
+    const int wib = threadIdx.x >> 5;
+    k1_body<2, true, true>(P, smem + wib * k1_warp_words<2, true>(),
+                           static_cast<long long>(blockIdx.x) * band::WARPS + wib, nullptr, nullptr);
 }
 
 template <int L> size_t smem_bytes() {
@@ -2370,6 +2434,15 @@ int launch_window_align(int L, const AlignParams& p, int grid, int warps_per_blo
         case 4: return launch_L<4>(p, grid, stream);
         default: return static_cast<int>(cudaErrorInvalidValue);
     }
+}
+
+int launch_tail_align(const AlignParams& p, int grid, void* stream) {
+    const size_t smem = static_cast<size_t>(band::WARPS) * k1_warp_words<2, true>() * 4;
+    cudaError_t e = cudaFuncSetAttribute(k1_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    k1_tail<<<grid, 32 * band::WARPS, smem, static_cast<cudaStream_t>(stream)>>>(p);
+    return static_cast<int>(cudaGetLastError());
 }
 
 int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream) {

@@ -88,6 +88,8 @@ struct AlignParams {
     int32_t* u_list;          // K0 (§3.10): pairs left to a full-frame K1 launch after the
     unsigned int* u_count;    // mixed one (unrelated pairs and every pair's tail windows)
     int32_t restore;          // the fresh pairs resume from resume_state (that launch)
+    int32_t* t_list;          // pairs whose next window is an STD window (m_w <= 31, the
+    unsigned int* t_count;    // pattern all but consumed): the tail K1 (k1_tail) after K1 mixed
     unsigned int* coop_out;   // pairs a band warp handed to a cooperative warp and not yet
                               // taken back (in q_coop, at a cooperative warp, or in q_band)
     // finished-pair counts per output slice (one-shot calls): a pair's run bytes and
@@ -127,6 +129,9 @@ int wide_max_blocks_per_sm();
 // windows of W <= 64 columns in diagonal coordinates) and full-frame warps
 // (limb count LF); pairs move between them through device queues.
 int launch_mixed_align(int LF, const AlignParams& p, int grid, void* stream);
+// The tail K1 (§3.10): band-type warps resume the pairs of p.order (their STD windows,
+// the standard single-word frame); any other window goes to p.u_list.
+int launch_tail_align(const AlignParams& p, int grid, void* stream);
 int launch_queue_init(uint32_t* q_band, uint32_t* q_full, uint32_t* q_coop, uint32_t* q_std,
                       unsigned* remaining, int n, const int32_t* n_dev, void* stream);
 
