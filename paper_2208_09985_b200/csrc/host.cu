@@ -1454,7 +1454,9 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             const int64_t sn = s.hi - s.lo;
             int slices = 0;
             int32_t per = 0;
-            if (sliced) {
+            // (K1 mixed finishes every pair with a tail window after its own launch,
+            // so no slice would be ready early: one K2/K3 and one D2H instead)
+            if (sliced && !rcs.band) {
                 slices = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices, std::max<int64_t>(1, sn / 4096)));
                 per = static_cast<int32_t>((sn + slices - 1) / slices);
                 slices = static_cast<int>((sn + per - 1) / per);
