@@ -527,10 +527,14 @@ bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) 
     if (kernel == SG_KERNEL_FULL) return false;
     const int64_t n = hi - lo;
     if (n <= 0) return false;
+    // the mixed kernel wins unless most pairs are a single final window (they go
+    // straight to the full-frame K1 after it) or many are unrelated (K0, §3.10).
+    // K1 on one B200, auto -> mixed: cfg2 9.4 -> 5.5 ms, cfg1 0.133 -> 0.103, cfg4 W=32
+    // 6.0 -> 5.5; cfg5 (30 % unrelated) stays full frame: 134 against 160 ms
     double tot = 0;
     for (int64_t k = lo; k < hi; ++k) tot += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
-    if (tot / static_cast<double>(n) / std::max(1, W - O) < 32.0) return false;
-    if (W <= 32) return false;  // one-limb full frame: no cheaper than the band (cfg4 W=32: 6.7 vs 7.0 ms)
+    if (tot / static_cast<double>(n) <= W) return false;
+    (void)O;
     const int64_t samples = std::min<int64_t>(n, 64);
     int tested = 0, unrelated = 0;
     for (int64_t i = 0; i < samples; ++i) {

@@ -341,16 +341,17 @@ def test_mixed_handoffs_terminate(gpu, set_options):
 
 @pytest.mark.gpu
 def test_kernel_choice(gpu):
-    """host.cu band_pays: long correlated reads run the mixed
-    kernel; short reads, W <= 32 and batches with many unrelated pairs the full
-    frame; W > 128 the wide kernel."""
+    """host.cu band_pays: correlated reads longer than a window
+    run the mixed kernel (W <= 64, W % 8 == 0); pairs of a single window, batches
+    with many unrelated pairs and W = 128 the full frame; W > 128 the wide kernel."""
     sg = gpu
     def kernel(cfg_id, count, W, Ov):
         return sg.Session(sg.AlignerConfig(W=W, O=Ov), sg.synth_packed(cfg_id, 0, count)).info()["kernel"]
     assert kernel(3, 2000, 64, 24) == "mixed"
     assert kernel(4, 500, 64, 33) == "mixed"
-    assert kernel(4, 500, 32, 12) == "full"
-    assert kernel(2, 2000, 64, 24) == "full"
+    assert kernel(4, 500, 32, 12) == "mixed"
+    assert kernel(2, 2000, 64, 24) == "mixed"
+    assert kernel(4, 200, 128, 48) == "full"
     assert kernel(5, 2000, 64, 24) == "full"
     assert kernel(4, 200, 256, 96) == "wide"
 
