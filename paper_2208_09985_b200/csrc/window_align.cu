@@ -968,9 +968,11 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                             ring[((hi + k) & 7) * 32 + lane] = have ? nx[k] : __ldcg(P.seq + hi + k);
                     hi = max(hi, need);
                 }
-                // the words the next window can add (it starts <= 3 words on)
+                // the words the next window can add (it starts <= 3 words on), issued
+                // here (volatile: not sunk towards their use a phase later)
 #pragma unroll
-                for (int k = 0; k < 3; ++k) nx[k] = __ldcg(P.seq + hi + k);
+                for (int k = 0; k < 3; ++k)
+                    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(nx[k]) : "l"(P.seq + hi + k));
                 pf = hi;
             };
             stage(sq_t, nx_t, nx_tw, pf_tw, wt);
@@ -1107,18 +1109,33 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 lut[(2 * c + 8) * 32] = make_uint2(0u, 0u);  // code c | 4
                 lut[(2 * c + 9) * 32] = make_uint2(0u, 0u);
             }
-            // EQ_i of every column (the parked row starts as row -1: zeros)
+            // EQ_i of every column (the parked row starts as row -1: zeros); the N
+            // bits only where a lane of the warp has a non-ACGT base
+            if (__any_sync(__activemask(), hasn)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (16 * k >= n_w) break;
-                const uint32_t tword = tw[k];
-                const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
+                for (int k = 0; k < 4; ++k) {
+                    if (16 * k >= n_w) break;
+                    const uint32_t tword = tw[k];
+                    const uint32_t tnw = hasn ? tn[k >> 1] >> (16 * (k & 1)) : 0u;
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int i = 16 * k + u;
-                    const uint32_t code = ((tword >> (2 * u)) & 3u) | (((tnw >> u) & 1u) << 2);
-                    const uint2 pr = lut[(2 * code + (i >> 5)) * 32];
-                    bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, i & 31), 0u);
+                    for (int u = 0; u < 16; ++u) {
+                        const int i = 16 * k + u;
+                        const uint32_t code = ((tword >> (2 * u)) & 3u) | (((tnw >> u) & 1u) << 2);
+                        const uint2 pr = lut[(2 * code + (i >> 5)) * 32];
+                        bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, i & 31), 0u);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (16 * k >= n_w) break;
+                    const uint32_t tword = tw[k];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int i = 16 * k + u;
+                        const uint2 pr = lut[(2 * ((tword >> (2 * u)) & 3u) + (i >> 5)) * 32];
+                        bmem.eqp[(i + 4) * 32] = make_uint2(__funnelshift_r(pr.x, pr.y, i & 31), 0u);
+                    }
                 }
             }
             // the parity planes of the window start at zero (the LUT above is dead)
@@ -1620,12 +1637,14 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                 const int dm = d0 + kBandR - 1;  // the window's last computed row
                 // the bit of (i + 1, j + 1): band j - i - e_lo, STD (tail K1) j + 1
                 int kb = TAIL ? 1 : -e_lo;
+                // table reads (dp.hpp:46-66): 3 per step while d > 0, 1 after; s0 =
+                // the step count when d reached 0
+                int s0 = d == 0 ? 0 : -1;
                 while (steps < lim && j < m_w) {
                     ++ph_steps;
                     ++tb_trip;
                     const int run = match_run(i, j);
                     const int k = min(run, min(lim - steps, m_w - j));
-                    reads += static_cast<unsigned>(k) * (d == 0 ? 1u : 3u);
                     i += k;
                     j += k;
                     steps += k;
@@ -1647,15 +1666,17 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
                     const uint32_t lt = (pl.x ^ (e0 - 1u)) & (pl.y ^ (e1 - 1u));  // D(nbr) == d - 1
                     const int op = (lt >> kb) & 1u ? 1 : (((lt << 1) >> kb) & 1u ? 3 : 2);
                     if (d == 0) status = kStInternal | kDetNoStep;
-                    reads += d == 0 ? 1u : 3u;
                     i += op != 2;
                     j += op != 3;
                     kb += (op == 2) - (op == 3);
                     --d;
                     ++dist;
                     ++steps;
+                    if (d == 0) s0 = steps;
                     emit_short(op, 1);
                 }
+                if (s0 < 0) s0 = steps;
+                reads += 2u * static_cast<unsigned>(s0) + static_cast<unsigned>(steps);
             } else
             for (;;) {
                 ++ph_steps;
