@@ -1,0 +1,7 @@
+# round-2 re-entry check of HEAD: GPU suite, driver-style bench, K1 phases, per-config ncu metrics
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2c_gpu_pytest.log 2>&1; echo "pytest rc=$?"
+timeout 900 python bench.py > gpurun_out/r2c_bench.json 2> gpurun_out/r2c_bench.err; echo "bench rc=$?"
+timeout 300 python scripts/profile_k1.py --cfg 3 --pairs 100000 --runs 3 --phases > gpurun_out/r2c_cfg3.log 2>&1
+TAG=r2c bash scripts/gpu/ncu_configs.sh
+tail -n 3 gpurun_out/r2c_gpu_pytest.log gpurun_out/r2c_cfg3.log
