@@ -21,13 +21,28 @@ constexpr unsigned kFull = 0xffffffffu;
 template <int L> struct KCfg;
 template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4, MINB = 2; };
 template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4, MINB = 3; };
-template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2, MINB = 1; };
+// (L = 4: C covers W - O = 80 of cfg4's W = 128, O = 48; with 32 columns every such
+// window ran as three continuation segments, 2.7 x the DC chunks)
+#ifndef SG_C4
+#define SG_C4 80
+#endif
+template <> struct KCfg<4> { static constexpr int R = 4, C = SG_C4, WARPS = 2, MINB = 1; };
 // DC chunks per state-machine iteration (traceback batching, see the main loop)
 // (band warps: their chunks cost a third of a full-frame chunk, so the traceback
 // and setup phases amortise over more of them; measured 2 / 3 / 4 / 6 / 8 on cfg3:
 // 4 is best)
 #ifndef SG_SUBCHUNKS
 #define SG_SUBCHUNKS 2
+#endif
+// Full-frame warps: after kSubChunks chunks the traceback phase starts once
+// kTbLanes of 32 (scaled to the lanes that hold a pair) wait for it, or after
+// kSubMax chunks. A window of an unrelated pair takes ~9 chunks: with a phase every
+// 2 chunks only ~18 % of the lanes were in each traceback.
+#ifndef SG_TB_LANES
+#define SG_TB_LANES 12
+#endif
+#ifndef SG_SUBMAX
+#define SG_SUBMAX 6
 #endif
 #ifndef SG_BAND_R
 #define SG_BAND_R 8  // rows per band chunk (kBandR)
@@ -36,6 +51,7 @@ template <> struct KCfg<4> { static constexpr int R = 4, C = 32, WARPS = 2, MINB
 #define SG_BAND_SUBCHUNKS (16 / SG_BAND_R)  // 16 rows per phase
 #endif
 constexpr int kSubChunks = SG_SUBCHUNKS;
+constexpr int kTbLanes = SG_TB_LANES, kSubMax = SG_SUBMAX < SG_SUBCHUNKS ? SG_SUBCHUNKS : SG_SUBMAX;
 constexpr int kBandSubChunks = SG_BAND_SUBCHUNKS;
 // (R = 4: sweep groups are aligned to 4-column text-code words; C % 4 == 0.)
 
@@ -1505,9 +1521,16 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         // Up to kSubChunks chunks of R rows before the traceback phase, so
         // that more lanes reach it together; solved lanes sweep idle.
         bool solved = false;
-        for (int sub = 0; sub < (BAND ? kBandSubChunks : kSubChunks); ++sub) {
+        const int n_in = BAND ? 0 : __popc(__ballot_sync(kFull, in_dc));
+        for (int sub = 0; sub < (BAND ? kBandSubChunks : kSubMax); ++sub) {
             const bool act = in_dc && !solved;
-            if (sub > 0 && !__any_sync(kFull, act)) break;
+            if (BAND) {
+                if (sub > 0 && !__any_sync(kFull, act)) break;
+            } else if (sub > 0) {
+                const int n_act = __popc(__ballot_sync(kFull, act));
+                if (n_act == 0) break;
+                if (sub >= kSubChunks && (n_in - n_act) * 32 >= n_in * kTbLanes) break;
+            }
             if constexpr (BAND) {
                 // (the main pass's band warps never hold an STD window: those are pair
                 // tails, run by the tail K1 in the STD frame, §3.10)
