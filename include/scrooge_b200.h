@@ -191,7 +191,9 @@ enum {
 enum {
     SG_DIAG_WARP_TIMES = 1,   /* per-warp start/exit timeline of sessions' K1 */
     SG_DIAG_PHASE_CYCLES = 2, /* per-phase SM cycles of sessions' K1 */
-    SG_DIAG_HOST_TRACE = 4    /* host pipeline timestamps on stderr */
+    SG_DIAG_HOST_TRACE = 4,   /* host pipeline timestamps on stderr */
+    SG_DIAG_NO_PIPELINE = 8   /* one-shot calls launch the mixed kernel's tail kernels after it,
+                                 not beside it: A/B and cross-checks */
 };
 typedef struct sg_options {
     int32_t kernel;         /* SG_KERNEL_* */

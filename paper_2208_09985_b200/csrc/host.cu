@@ -18,6 +18,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/scrooge_b200.h"
@@ -68,7 +69,93 @@ int hw_threads() {
     return h ? static_cast<int>(std::min(h, 64u)) : 8;
 }
 
-// f(lo, hi, thread_index) over [0, n) in contiguous chunks.
+// Worker threads for the host loops over the pairs, started once and kept (creating
+// a thread costs ~0.2 ms on the GPU hosts: more than a pass over 100 k pairs). One
+// parallel loop uses them at a time; a caller that finds them busy (another shard's
+// host thread) runs its loop on threads of its own.
+class WorkerPool {
+  public:
+    explicit WorkerPool(int workers) {
+        for (int w = 0; w < workers; ++w) std::thread([this] { loop(); }).detach();
+    }
+    // job(t) for t in [0, tasks), the caller taking part; false when the pool is busy
+    template <class Job>
+    bool run(int tasks, Job&& job) {
+        std::unique_lock<std::mutex> use(use_mu_, std::try_to_lock);
+        if (!use.owns_lock()) return false;
+        using JobT = typename std::remove_reference<Job>::type;
+        struct Call {
+            JobT* job;
+            static void invoke(void* c, int t) { (*static_cast<Call*>(c)->job)(t); }
+        } call{&job};
+        unsigned gen;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &Call::invoke;
+            ctx_ = &call;
+            tasks_ = tasks;
+            gen = ++gen_;
+            next_.store(static_cast<uint64_t>(gen) << 32);
+            left_ = tasks;
+        }
+        cv_.notify_all();
+        drain(gen, tasks, &Call::invoke, &call);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return left_ == 0; });
+        fn_ = nullptr;
+        return true;
+    }
+
+  private:
+    // Tasks of generation `gen` only: the ticket carries the generation, so a worker
+    // that wakes late never takes (or skips) a task of a later loop.
+    void drain(unsigned gen, int tasks, void (*fn)(void*, int), void* ctx) {
+        uint64_t cur = next_.load();
+        for (;;) {
+            if (static_cast<unsigned>(cur >> 32) != gen || static_cast<int>(cur & 0xFFFFFFFFu) >= tasks)
+                return;
+            if (!next_.compare_exchange_weak(cur, cur + 1)) continue;
+            fn(ctx, static_cast<int>(cur & 0xFFFFFFFFu));
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--left_ == 0) done_.notify_all();
+            }
+            cur = next_.load();
+        }
+    }
+    void loop() {
+        unsigned seen = 0;
+        for (;;) {
+            void (*fn)(void*, int);
+            void* ctx;
+            int tasks;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen && fn_ != nullptr; });
+                seen = gen_;
+                fn = fn_;
+                ctx = ctx_;
+                tasks = tasks_;
+            }
+            drain(seen, tasks, fn, ctx);
+        }
+    }
+    std::mutex use_mu_, mu_;
+    std::condition_variable cv_, done_;
+    void (*fn_)(void*, int) = nullptr;
+    void* ctx_ = nullptr;
+    int tasks_ = 0, left_ = 0;
+    std::atomic<uint64_t> next_{0};  // (generation << 32) | next task
+    unsigned gen_ = 0;
+};
+
+WorkerPool& worker_pool() {  // (leaked: its threads never outlive a destroyed object)
+    static WorkerPool* pool = new WorkerPool(std::max(1, hw_threads() - 1));
+    return *pool;
+}
+
+// f(lo, hi, chunk_index) over [0, n) in contiguous chunks (at most 64, at least
+// `grain` items each).
 template <class F>
 void parallel_for(int64_t n, F&& f, int64_t grain = 1024) {
     int threads = hw_threads();
@@ -77,13 +164,14 @@ void parallel_for(int64_t n, F&& f, int64_t grain = 1024) {
         f(int64_t{0}, n, 0);
         return;
     }
-    std::vector<std::thread> pool;
     const int64_t chunk = (n + threads - 1) / threads;
-    for (int t = 0; t < threads; ++t) {
+    auto task = [&](int t) {
         const int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
-        if (lo >= hi) break;
-        pool.emplace_back([&f, lo, hi, t] { f(lo, hi, t); });
-    }
+        if (lo < hi) f(lo, hi, t);
+    };
+    if (worker_pool().run(threads, task)) return;
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back([&task, t] { task(t); });
     for (auto& th : pool) th.join();
 }
 
@@ -225,6 +313,7 @@ struct DevState {
     cudaEvent_t copy_go = nullptr;
     cudaEvent_t copy_done = nullptr; // the last piece of the upload (joined before K2)
     int64_t chunk_words = 1;
+    int n_chunks = 1;                // pieces of the last sequence upload
     DevBuf dense_off, dense, scan_tmp;
     DevBuf ex_store, ex_hbuf, ex_store_off, ex_hbuf_off;  // K7 (exact global alignment)
     // K1 mixed (§3.8-3.10): hand-over queues, counters (remaining pairs, K0 count),
@@ -238,6 +327,14 @@ struct DevState {
     // own stream while K1 runs, each slice's run bytes copied out as soon as it is ready
     static constexpr int kMaxSlices = 32;
     DevBuf slice_done;
+    // pipelined launches of the mixed kernel (§3.12): per-slice list counts, hand-over
+    // counts, queue heads and the error flag (kPipe* offsets, in 32-bit words)
+    DevBuf pipe_ctr;
+    static constexpr int kPipeT = 0, kPipeU = kMaxSlices, kPipeBody = 2 * kMaxSlices,
+                         kPipeTailQ = 3 * kMaxSlices, kPipeFullQ = 4 * kMaxSlices,
+                         kPipeErr = 5 * kMaxSlices, kPipeWords = 5 * kMaxSlices + 8;
+    int tail_sms = 0;               // SMs the last pipelined launch left to the tail kernels
+    cudaEvent_t k1_done = nullptr;  // the last slice's full-frame K1 (K1's end in a pipelined launch)
     cudaStream_t slice_stream = nullptr, d2h = nullptr;
     cudaEvent_t slice_go = nullptr, slices_done = nullptr, ev_slice[kMaxSlices] = {};
     int64_t* slice_info = nullptr;  // host-mapped [2 * kMaxSlices]: (first byte, bytes)
@@ -255,6 +352,7 @@ struct DevState {
         SG_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
         SG_CUDA_CHECK(cudaEventCreateWithFlags(&slice_go, cudaEventDisableTiming));
         SG_CUDA_CHECK(cudaEventCreateWithFlags(&slices_done, cudaEventDisableTiming));
+        SG_CUDA_CHECK(cudaEventCreateWithFlags(&k1_done, cudaEventDisableTiming));
         for (auto& e : ev_slice) SG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         void* info = nullptr;
         SG_CUDA_CHECK(cudaHostAlloc(&info, 16 * kMaxSlices, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -269,8 +367,9 @@ struct DevState {
                           &scratch, &bnd, &next_pair, &ready, &bnd_ones, &bnd_zeros, &dense_off,
                           &dense, &scan_tmp, &ex_store, &ex_hbuf, &ex_store_off, &ex_hbuf_off,
                           &q_band, &q_full, &q_coop, &q_std, &mixed_ctr, &resume_state, &t_list,
-                          &u_list, &diag_warp, &diag_phase, &slice_done})
+                          &u_list, &diag_warp, &diag_phase, &slice_done, &pipe_ctr})
             b->release();
+        if (k1_done) cudaEventDestroy(k1_done);
         if (slice_stream) cudaStreamDestroy(slice_stream);
         if (d2h) cudaStreamDestroy(d2h);
         if (slice_go) cudaEventDestroy(slice_go);
@@ -328,22 +427,37 @@ int validate_cfg(const sg_config* c) {
 
 constexpr int64_t kMaxSingle = 1024;     // BitVector::kMaxBits (bitvec.hpp:29)
 
+// Host loops over the pairs run on several threads from this batch size on (a
+// cfg2-sized call has 1 M pairs: each serial pass over them costs 1-7 ms).
+constexpr int64_t kParGrain = 8192;
+
 int validate_lengths(int64_t n, const int64_t* tl, const int64_t* pl, const sg_config* c) {
-    for (int64_t k = 0; k < n; ++k) {
-        if (tl[k] <= 0 || pl[k] <= 0)  // batch.cpp:18-25
-            return set_error(SG_INPUT, "pair '%lld': empty sequence", static_cast<long long>(k));
-        if (tl[k] + pl[k] > (int64_t{1} << 30))
-            return set_error(SG_INPUT, "pair '%lld': sequence too long for one GPU pair slot",
-                             static_cast<long long>(k));
-        if (c->single_window) {
-            // aligner.cpp:92-94; run_batch reports it as an input error (batch.cpp:94-97)
-            if (tl[k] > kMaxSingle || pl[k] > kMaxSingle)
-                return set_error(SG_INPUT,
-                                 "pair '%lld': single-window mode requires sequences of at most "
-                                 "1024 characters", static_cast<long long>(k));
-        }
+    // kind of the first (lowest-index) bad pair: 1 empty, 2 too long, 3 single-window cap
+    auto check = [&](int64_t k) -> int {
+        if (tl[k] <= 0 || pl[k] <= 0) return 1;  // batch.cpp:18-25
+        if (tl[k] + pl[k] > (int64_t{1} << 30)) return 2;
+        // aligner.cpp:92-94; run_batch reports it as an input error (batch.cpp:94-97)
+        if (c->single_window && (tl[k] > kMaxSingle || pl[k] > kMaxSingle)) return 3;
+        return 0;
+    };
+    std::vector<int64_t> first(64, INT64_MAX);
+    parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
+        for (int64_t k = lo; k < hi; ++k)
+            if (check(k)) {
+                first[static_cast<size_t>(t)] = k;
+                break;
+            }
+    }, kParGrain);
+    const int64_t bad = *std::min_element(first.begin(), first.end());
+    if (bad == INT64_MAX) return SG_OK;
+    switch (check(bad)) {
+        case 1: return set_error(SG_INPUT, "pair '%lld': empty sequence", static_cast<long long>(bad));
+        case 2: return set_error(SG_INPUT, "pair '%lld': sequence too long for one GPU pair slot",
+                                 static_cast<long long>(bad));
+        default: return set_error(SG_INPUT,
+                                  "pair '%lld': single-window mode requires sequences of at most "
+                                  "1024 characters", static_cast<long long>(bad));
     }
-    return SG_OK;
 }
 
 // ------------------------------------------------------------ packing (K4)
@@ -531,8 +645,15 @@ bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) 
     // straight to the full-frame K1 after it) or many are unrelated (K0, §3.10).
     // K1 on one B200, auto -> mixed: cfg2 9.4 -> 5.5 ms, cfg1 0.133 -> 0.103, cfg4 W=32
     // 6.0 -> 5.5; cfg5 (30 % unrelated) stays full frame: 134 against 160 ms
+    std::vector<double> part(64, 0.0);
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+        double acc = 0;
+        for (int64_t k = lo + a; k < lo + b; ++k)
+            acc += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
+        part[static_cast<size_t>(t)] = acc;
+    }, kParGrain);
     double tot = 0;
-    for (int64_t k = lo; k < hi; ++k) tot += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
+    for (double v : part) tot += v;
     if (tot / static_cast<double>(n) <= W) return false;
     (void)O;
     const int64_t samples = std::min<int64_t>(n, 64);
@@ -556,35 +677,54 @@ struct ShardPrep {
     bool ordered = false;
 };
 
-bool any_bits(const uint32_t* m, int64_t base, int64_t len) {
-    for (int64_t k = 0; k < len; ++k) {
-        const int64_t b = base + k;
-        if ((m[b >> 5] >> (b & 31)) & 1u) return true;
-    }
-    return false;
+bool any_bits(const uint32_t* m, int64_t base, int64_t len) {  // any of bits [base, base + len)
+    if (len <= 0) return false;
+    const int64_t end = base + len;
+    int64_t w = base >> 5;
+    const int64_t wl = (end - 1) >> 5;
+    uint32_t first = ~0u << (base & 31);
+    const uint32_t last = ~0u >> (31 - ((end - 1) & 31));
+    if (w == wl) return (m[w] & first & last) != 0u;
+    if (m[w] & first) return true;
+    for (++w; w < wl; ++w)
+        if (m[w]) return true;
+    return (m[wl] & last) != 0u;
 }
 
 // Packed words a shard's pairs use: [lo, hi), lo even (the N mask stays 32-bit
 // aligned after rebasing).
 void shard_words(const Shard& s, int64_t* lo, int64_t* hi) {
     const sg_packed_pairs* in = s.in;
-    int64_t wlo = INT64_MAX, whi = 0;
-    for (int64_t k = s.lo; k < s.hi; ++k) {
-        wlo = std::min({wlo, in->text_off[k] >> 4, in->pat_off[k] >> 4});
-        whi = std::max({whi, (in->text_off[k] + in->text_len[k] + 15) >> 4,
-                        (in->pat_off[k] + in->pat_len[k] + 15) >> 4});
-    }
+    std::vector<int64_t> plo(64, INT64_MAX), phi(64, 0);
+    parallel_for(s.hi - s.lo, [&](int64_t a, int64_t b, int t) {
+        int64_t l = INT64_MAX, h = 0;
+        for (int64_t k = s.lo + a; k < s.lo + b; ++k) {
+            l = std::min({l, in->text_off[k] >> 4, in->pat_off[k] >> 4});
+            h = std::max({h, (in->text_off[k] + in->text_len[k] + 15) >> 4,
+                          (in->pat_off[k] + in->pat_len[k] + 15) >> 4});
+        }
+        plo[static_cast<size_t>(t)] = l;
+        phi[static_cast<size_t>(t)] = h;
+    }, kParGrain);
+    int64_t wlo = *std::min_element(plo.begin(), plo.end());
+    int64_t whi = *std::max_element(phi.begin(), phi.end());
     if (s.hi <= s.lo) wlo = whi = 0;
     *lo = wlo & ~int64_t{1};
     *hi = whi;
 }
 
-void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split = 0) {
+void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split = 0,
+                const int64_t* words = nullptr) {
     const sg_packed_pairs* in = s.in;
     const int64_t n = s.hi - s.lo;
     pp.n = n;
     int64_t wlo = 0, whi = 0;
-    shard_words(s, &wlo, &whi);
+    if (words) {
+        wlo = words[0];
+        whi = words[1];
+    } else {
+        shard_words(s, &wlo, &whi);
+    }
     pp.word_lo = wlo;
     pp.word_hi = whi;
     const int64_t rebase = wlo * 16;
@@ -595,26 +735,44 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split
     pp.pat_len.ensure(4 * n1);
     pp.has_n.ensure(n1);
     pp.bound_off.ensure(8 * n1);
-    int64_t bound = 0;
-    bool any_n = false;
-    for (int64_t k = 0; k < n; ++k) {
-        const int64_t g = s.lo + k;
-        pp.text_off.as<int64_t>()[k] = in->text_off[g] - rebase;
-        pp.pat_off.as<int64_t>()[k] = in->pat_off[g] - rebase;
-        pp.text_len.as<int32_t>()[k] = static_cast<int32_t>(in->text_len[g]);
-        pp.pat_len.as<int32_t>()[k] = static_cast<int32_t>(in->pat_len[g]);
-        bool hn = false;
-        if (in->nmask)
-            hn = any_bits(in->nmask, in->text_off[g], in->text_len[g]) ||
-                 any_bits(in->nmask, in->pat_off[g], in->pat_len[g]);
-        pp.has_n.as<uint8_t>()[k] = hn;
-        any_n |= hn;
-        pp.bound_off.as<int64_t>()[k] = bound;
-        // at most one run byte per edit op, ops <= n + m
-        bound += ((in->text_len[g] + in->pat_len[g] + 3) & ~int64_t{3}) + 4;
-    }
-    pp.any_n = any_n;
-    pp.scratch_bytes = bound;
+    // run-byte bound of a pair: at most one byte per edit op, ops <= n + m
+    auto bound_of = [&](int64_t g) {
+        return ((in->text_len[g] + in->pat_len[g] + 3) & ~int64_t{3}) + 4;
+    };
+    // two passes over contiguous chunks: each chunk's bound total, then its pairs
+    // from the chunk's base
+    std::vector<int64_t> cbound(65, 0), clo(64, 0), chi(64, 0);
+    std::vector<uint8_t> cn(64, 0);
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+        int64_t acc = 0;
+        for (int64_t k = a; k < b; ++k) acc += bound_of(s.lo + k);
+        cbound[static_cast<size_t>(t) + 1] = acc;
+        clo[static_cast<size_t>(t)] = a;
+        chi[static_cast<size_t>(t)] = b;
+    }, kParGrain);
+    for (size_t t = 0; t < 64; ++t) cbound[t + 1] += cbound[t];
+    parallel_for(n, [&](int64_t a, int64_t b, int t) {
+        int64_t bound = cbound[static_cast<size_t>(t)];
+        bool any = false;
+        for (int64_t k = a; k < b; ++k) {
+            const int64_t g = s.lo + k;
+            pp.text_off.as<int64_t>()[k] = in->text_off[g] - rebase;
+            pp.pat_off.as<int64_t>()[k] = in->pat_off[g] - rebase;
+            pp.text_len.as<int32_t>()[k] = static_cast<int32_t>(in->text_len[g]);
+            pp.pat_len.as<int32_t>()[k] = static_cast<int32_t>(in->pat_len[g]);
+            bool hn = false;
+            if (in->nmask)
+                hn = any_bits(in->nmask, in->text_off[g], in->text_len[g]) ||
+                     any_bits(in->nmask, in->pat_off[g], in->pat_len[g]);
+            pp.has_n.as<uint8_t>()[k] = hn;
+            any |= hn;
+            pp.bound_off.as<int64_t>()[k] = bound;
+            bound += bound_of(g);
+        }
+        cn[static_cast<size_t>(t)] = any;
+    }, kParGrain);
+    pp.any_n = std::any_of(cn.begin(), cn.end(), [](uint8_t v) { return v != 0; });
+    pp.scratch_bytes = cbound[64];
     pp.ordered = longest_first && n > 1 && options().longest_first;
     if (pp.ordered) {
         pp.order.ensure(4 * static_cast<size_t>(n));
@@ -688,11 +846,13 @@ RunConfig run_config(const sg_config* c, int64_t n = 0, const int64_t* tl = null
     return r;
 }
 
-// Sequence words go in kChunks pieces. Streamed (one-shot calls): the pieces
+// Sequence words go in up to kChunks pieces of at least 2 MB (a small batch is one
+// piece: every piece costs two API calls before K1 can launch). Streamed (one-shot calls): the pieces
 // go on the copy stream, each followed by its ready flag, while K1 already runs
 // on the main stream; a lane waits for the piece holding its pair's last word
 // (K1 fetch). Otherwise (sessions) everything is copied and flagged up front.
 constexpr int kChunks = 16;
+constexpr int64_t kChunkMinWords = int64_t{1} << 19;
 
 // The sequence words (the bulk of the H2D), issued before the host prepares the
 // per-pair arrays so that they arrive earlier (one-shot calls stream them, §1).
@@ -704,7 +864,8 @@ int64_t upload_seq(DevState& st, const Shard& s, int64_t word_lo, int64_t word_h
     st.seq.ensure(seq_bytes);
     st.ready.ensure(4 * kChunks);
     const int64_t avail = std::max<int64_t>(0, std::min<int64_t>(words + 48, in->seq_words - word_lo));
-    st.chunk_words = std::max<int64_t>(1, (avail + kChunks - 1) / kChunks);
+    st.n_chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kChunks, avail / kChunkMinWords)));
+    st.chunk_words = std::max<int64_t>(1, (avail + st.n_chunks - 1) / st.n_chunks);
     cudaStream_t cs = streamed ? st.copy : st.stream;
     SG_CUDA_CHECK(cudaMemsetAsync(st.ready.p, 0, 4 * kChunks, st.stream));
     if (streamed) {
@@ -714,7 +875,7 @@ int64_t upload_seq(DevState& st, const Shard& s, int64_t word_lo, int64_t word_h
     if (static_cast<size_t>(4 * avail) < seq_bytes)
         SG_CUDA_CHECK(cudaMemsetAsync(static_cast<char*>(st.seq.p) + 4 * avail, 0,
                                       seq_bytes - 4 * static_cast<size_t>(avail), cs));
-    for (int c = 0; c < kChunks; ++c) {
+    for (int c = 0; c < st.n_chunks; ++c) {
         const int64_t lo = std::min<int64_t>(avail, c * st.chunk_words);
         const int64_t hi = std::min<int64_t>(avail, lo + st.chunk_words);
         if (hi > lo) {
@@ -797,9 +958,9 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
 // full-frame kernel, whole rounds do not pay here (cfg3 100k: 3.02 rounds on all
 // 1036 warps 28.7 ms, 4 whole rounds on 782 warps 33.7 ms) — the last pairs run
 // on nearly idle SMs and hand their tails to the cooperative warps.
-long long band_active_warps(const DevState& st, const RunConfig& rc, int64_t n) {
+long long band_active_warps(const DevState& st, const RunConfig& rc, int64_t n, int sms = 0) {
     (void)rc;
-    const long long max_warps = static_cast<long long>(st.sms) * sgk::mixed_band_warps();
+    const long long max_warps = static_cast<long long>(sms > 0 ? sms : st.sms) * sgk::mixed_band_warps();
     const long long w = (static_cast<long long>(n) + 31) / 32;
     return std::max(1LL, std::min(w, max_warps));
 }
@@ -809,6 +970,27 @@ int64_t pairs_in_flight(const DevState& st, const RunConfig& rc, int64_t n) {
     if (rc.band) return band_active_warps(st, rc, n) * 32;
     const long long g = k1_grid(st, rc, n);
     return rc.wide ? g * sgk::wide_warps_per_block() : g * sgk::k1_warps_per_block(rc.L) * 32;
+}
+
+// Pipelined launches (§3.12): the SMs K1 mixed leaves to the tail K1 and the full-frame
+// K1 of the slices, in proportion to the work they get. In band-window units (cfg3 /
+// cfg2 on one B200: 0.096 SM-us per band window) an STD window of a pair's tail costs
+// ~7 (D ~ 48 in the 32-bit standard frame) and a final window in the full-frame K1
+// ~2.65. From a strided sample of the pairs; only the split depends on it.
+int tail_sm_count(const DevState& st, const RunConfig& rc, const ShardPrep& pp) {
+    const int64_t n = pp.n;
+    const int64_t samples = std::min<int64_t>(n, 4096);
+    const double step = std::max(1, rc.W - rc.O);
+    double band = 0, tail = 0;
+    for (int64_t i = 0; i < samples; ++i) {
+        const int64_t k = i * n / samples;
+        const double tl = pp.text_len.as<int32_t>()[k], pl = pp.pat_len.as<int32_t>()[k];
+        band += std::max(0.0, std::max(tl, pl) - rc.W) / step;
+        tail += tl - pl >= 32 ? 7.0 : 2.65;
+    }
+    const double share = tail / std::max(1.0, band + tail);
+    const int t = static_cast<int>(std::ceil(1.1 * share * st.sms));
+    return std::max(2, std::min(t, st.sms / 2));
 }
 
 // Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
@@ -832,8 +1014,13 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
     const long long grid = k1_grid(st, rc, n);
     st.grid = grid;
     st.lanes = grid * wpb * (rc.wide ? 1 : 32);  // pairs in flight
-    const long long band_warps = rc.band ? band_active_warps(st, rc, n) : 0;
-    const long long grid_band = rc.band ? std::min<long long>(st.sms, band_warps) : 0;
+    // pipelined (§3.12): K1 mixed on all SMs but `tsm`, the slices' tail / full-frame K1
+    // and K2 / K3 beside it on the slice stream
+    const bool piped = rc.band && slices > 0;
+    const int tsm = piped ? tail_sm_count(st, rc, pp) : 0;
+    st.tail_sms = tsm;
+    const long long band_warps = rc.band ? band_active_warps(st, rc, n, st.sms - tsm) : 0;
+    const long long grid_band = rc.band ? std::min<long long>(st.sms - tsm, band_warps) : 0;
     if (rc.band) {
         st.lanes = band_warps * 32;
         st.q_band.ensure(4 * (n1 + 32));
@@ -884,7 +1071,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
     p.next_pair = st.next_pair.as<unsigned int>();
     p.ready = st.ready.as<unsigned int>();
     p.chunk_words = st.chunk_words;
-    p.n_chunks = kChunks;
+    p.n_chunks = st.n_chunks;
     p.wcap = rc.wcap;
     p.phase_cycles = nullptr;
     p.warp_times = nullptr;
@@ -907,9 +1094,14 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
         st.slice_done.ensure(4 * DevState::kMaxSlices);
         SG_CUDA_CHECK(cudaMemsetAsync(st.slice_done.p, 0, 4 * DevState::kMaxSlices, st.stream));
         SG_CUDA_CHECK(cudaMemsetAsync(st.dense_off.p, 0, 8, st.stream));
-        p.slice_done = st.slice_done.as<unsigned int>();
+        p.slice_done = piped ? nullptr : st.slice_done.as<unsigned int>();
         p.slice_pairs = slice_pairs;
-        SG_CUDA_CHECK(cudaEventRecord(st.slice_go, st.stream));
+        if (piped) {
+            st.pipe_ctr.ensure(4 * DevState::kPipeWords);
+            SG_CUDA_CHECK(cudaMemsetAsync(st.pipe_ctr.p, 0, 4 * DevState::kPipeWords, st.stream));
+        } else {
+            SG_CUDA_CHECK(cudaEventRecord(st.slice_go, st.stream));
+        }
     }
     int launches = 0;
     SG_CUDA_CHECK(cudaEventRecord(st.ev[0], st.stream));
@@ -941,6 +1133,77 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
         p.t_count = st.mixed_ctr.as<unsigned int>() + 10;
         p.u_list = st.u_list.as<int32_t>();
         p.u_count = st.mixed_ctr.as<unsigned int>() + 8;
+        if (piped) {
+            unsigned int* ctr = st.pipe_ctr.as<unsigned int>();
+            p.t_count = ctr + DevState::kPipeT;
+            p.u_count = ctr + DevState::kPipeU;
+            p.body_done = ctr + DevState::kPipeBody;
+            p.last_slice = slices - 1;
+            p.pipe_err = ctr + DevState::kPipeErr;
+            // everything the slice stream's kernels read is set up before they start
+            SG_CUDA_CHECK(cudaEventRecord(st.slice_go, st.stream));
+            SG_CUDA_CHECK(cudaStreamWaitEvent(st.slice_stream, st.slice_go, 0));
+            SG_CUDA_CHECK(static_cast<cudaError_t>(
+                sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
+            ++launches;
+            const int full_bps = std::max(1, sgk::k1_max_blocks_per_sm(rc.L));
+            int64_t* info = nullptr;
+            SG_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&info), st.slice_info, 0));
+            for (int sl = 0; sl < slices; ++sl) {
+                const int32_t lo = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl} * slice_pairs));
+                const bool last = sl == slices - 1;
+                const int32_t hi = last ? static_cast<int32_t>(n)
+                                        : static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl + 1} * slice_pairs));
+                // the slice's STD windows, once its pairs have left K1 mixed: on the SMs
+                // K1 mixed leaves free (the last slice: on every SM, K1 mixed is ending)
+                sgk::AlignParams pt = p;
+                pt.warp_times = nullptr;
+                pt.mixed = 0;
+                pt.body_done = nullptr;
+                pt.t_list = nullptr;
+                pt.order = st.t_list.as<int32_t>() + lo;
+                pt.n_fresh = reinterpret_cast<const int32_t*>(ctr + DevState::kPipeT + sl);
+                pt.next_pair = ctr + DevState::kPipeTailQ + sl;
+                pt.restore = 1;
+                pt.band_active = 0x7FFFFFFF;
+                pt.u_list = st.u_list.as<int32_t>() + lo;
+                pt.u_count = ctr + DevState::kPipeU + sl;
+                pt.wait_count = ctr + DevState::kPipeBody + sl;
+                pt.wait_target = static_cast<unsigned>(hi - lo);
+                SG_CUDA_CHECK(static_cast<cudaError_t>(
+                    sgk::launch_tail_align(pt, last ? st.sms : tsm, st.slice_stream)));
+                // then the full-frame K1 over the slice's list: final windows, unrelated pairs
+                sgk::AlignParams pu = p;
+                pu.warp_times = nullptr;
+                pu.mixed = 0;
+                pu.body_done = nullptr;
+                pu.u_list = nullptr;
+                pu.t_list = nullptr;
+                pu.order = st.u_list.as<int32_t>() + lo;
+                pu.n_fresh = reinterpret_cast<const int32_t*>(ctr + DevState::kPipeU + sl);
+                pu.next_pair = ctr + DevState::kPipeFullQ + sl;
+                pu.restore = 1;
+                const long long gfull = last ? grid : std::min<long long>(grid, static_cast<long long>(tsm) * full_bps);
+                SG_CUDA_CHECK(static_cast<cudaError_t>(
+                    sgk::launch_window_align(rc.L, pu, static_cast<int>(gfull), wpb, st.slice_stream)));
+                if (last) SG_CUDA_CHECK(cudaEventRecord(st.k1_done, st.slice_stream));
+                SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_slice_scan(
+                    st.out_bytes.as<int32_t>(), st.dense_off.as<int64_t>(), lo, hi, nullptr, sl, info,
+                    st.slice_stream)));
+                SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_slice_compact(
+                    st.scratch.as<uint32_t>(), st.bound_off.as<int64_t>(), st.dense_off.as<int64_t>(),
+                    st.out_bytes.as<int32_t>(), st.dense.as<uint8_t>(), lo, hi, st.slice_stream)));
+                SG_CUDA_CHECK(cudaEventRecord(st.ev_slice[sl], st.slice_stream));
+                launches += hi > lo ? 4 : 3;
+            }
+            SG_CUDA_CHECK(cudaEventRecord(st.slices_done, st.slice_stream));
+            SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.k1_done, 0));
+            SG_CUDA_CHECK(cudaEventRecord(st.ev[1], st.stream));
+            SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.copy_done, 0));
+            SG_CUDA_CHECK(cudaStreamWaitEvent(st.stream, st.slices_done, 0));
+            SG_CUDA_CHECK(cudaEventRecord(st.ev[2], st.stream));
+            return launches + 1;  // + the queue init
+        }
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_mixed_align(rc.L, p, static_cast<int>(grid_band), st.stream)));
         // the tail K1: the pairs' STD windows in the band warps' single-word frame
@@ -1010,7 +1273,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
 
 // Small per-pair outputs of a shard, staged in pinned memory.
 struct ShardOut {
-    PinBuf dist, win, status, doff, cnt;
+    PinBuf dist, win, status, doff, cnt, pipe_err;
     PinBuf runs;          // sliced calls: the run bytes, already copied out
     bool staged = false;
     int64_t run_bytes = 0;
@@ -1023,7 +1286,9 @@ struct ShardOut {
     int64_t h2d_bytes = 0, d2h_bytes = 0;
 };
 
-void fetch_small(DevState& st, int64_t n, ShardOut& so) {
+// Issues the D2H of a shard's small per-pair outputs on its main stream (they wait
+// for every kernel there); fetch_small_finish waits for them.
+void fetch_small_issue(DevState& st, int64_t n, ShardOut& so) {
     const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
     so.dist.ensure(4 * n1);
     so.win.ensure(4 * n1);
@@ -1042,19 +1307,44 @@ void fetch_small(DevState& st, int64_t n, ShardOut& so) {
     d2h(so.status, st.status, 4 * un);
     d2h(so.doff, st.dense_off, 8 * (un + 1));
     d2h(so.cnt, st.counters, 8 * SG_CNT_COUNT * un);
+    so.pipe_err.ensure(4);
+    *so.pipe_err.as<unsigned>() = 0;
+    if (st.tail_sms > 0)
+        SG_CUDA_CHECK(cudaMemcpyAsync(so.pipe_err.p, st.pipe_ctr.as<unsigned>() + DevState::kPipeErr, 4,
+                                      cudaMemcpyDeviceToHost, st.stream));
+}
+
+void fetch_small_finish(DevState& st, int64_t n, ShardOut& so) {
     SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+    if (*so.pipe_err.as<unsigned>()) {
+        set_error(SG_INTERNAL, "device pipeline: a slice's tail launch timed out waiting for K1 mixed");
+        throw Fail{SG_INTERNAL};
+    }
     so.run_bytes = so.doff.as<int64_t>()[n];
-    for (int64_t k = 0; k < n; ++k)
-        if (so.status.as<int32_t>()[k] != 0) {
-            so.first_bad = k;
-            so.first_bad_status = so.status.as<int32_t>()[k];
-            break;
-        }
+    std::vector<int64_t> bad(64, INT64_MAX);
+    parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
+        const int32_t* stp = so.status.as<int32_t>();
+        for (int64_t k = lo; k < hi; ++k)
+            if (stp[k] != 0) {
+                bad[static_cast<size_t>(t)] = k;
+                break;
+            }
+    }, kParGrain);
+    const int64_t fb = *std::min_element(bad.begin(), bad.end());
+    if (fb != INT64_MAX) {
+        so.first_bad = fb;
+        so.first_bad_status = so.status.as<int32_t>()[fb];
+    }
     float ms = 0, k1 = 0;
     SG_CUDA_CHECK(cudaEventElapsedTime(&ms, st.ev[0], st.ev[2]));
     SG_CUDA_CHECK(cudaEventElapsedTime(&k1, st.ev[0], st.ev[1]));
     so.device_ms = ms;
     so.k1_ms = k1;
+}
+
+void fetch_small(DevState& st, int64_t n, ShardOut& so) {
+    fetch_small_issue(st, n, so);
+    fetch_small_finish(st, n, so);
 }
 
 // The sliced D2H (§5): slice by slice, as soon as K2/K3 have made its bytes dense,
@@ -1107,22 +1397,31 @@ void scatter_small(sg_results* out, int64_t base, int64_t n, int64_t run_base, c
     const int32_t* dist = so.dist.as<int32_t>();
     const int32_t* win = so.win.as<int32_t>();
     const int64_t* doff = so.doff.as<int64_t>();
-    for (int64_t k = 0; k < n; ++k) {
-        out->distance[base + k] = dist[k];
-        out->windows[base + k] = win[k];
-        out->found[base + k] = dist[k] >= 0;  // single window: D > k is "not found"
-        out->cigar_off[base + k] = run_base + doff[k];
-    }
+    parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+        for (int64_t k = lo; k < hi; ++k) {
+            out->distance[base + k] = dist[k];
+            out->windows[base + k] = win[k];
+            out->found[base + k] = dist[k] >= 0;  // single window: D > k is "not found"
+            out->cigar_off[base + k] = run_base + doff[k];
+        }
+        std::memcpy(out->counters + (base + lo) * SG_CNT_COUNT, so.cnt.as<uint64_t>() + lo * SG_CNT_COUNT,
+                    8 * SG_CNT_COUNT * static_cast<size_t>(hi - lo));
+    }, kParGrain);
     out->cigar_off[base + n] = run_base + doff[n];
-    if (n)
-        std::memcpy(out->counters + base * SG_CNT_COUNT, so.cnt.p,
-                    8 * SG_CNT_COUNT * static_cast<size_t>(n));
 }
 
 void finish_totals(sg_results* out) {
-    for (int c = 0; c < SG_CNT_COUNT; ++c) out->total[c] = 0;
-    for (int64_t k = 0; k < out->n_pairs; ++k)
-        for (int c = 0; c < SG_CNT_COUNT; ++c) out->total[c] += out->counters[k * SG_CNT_COUNT + c];
+    std::vector<uint64_t> part(64 * SG_CNT_COUNT, 0);
+    parallel_for(out->n_pairs, [&](int64_t lo, int64_t hi, int t) {
+        uint64_t acc[SG_CNT_COUNT] = {};
+        for (int64_t k = lo; k < hi; ++k)
+            for (int c = 0; c < SG_CNT_COUNT; ++c) acc[c] += out->counters[k * SG_CNT_COUNT + c];
+        for (int c = 0; c < SG_CNT_COUNT; ++c) part[static_cast<size_t>(t) * SG_CNT_COUNT + c] = acc[c];
+    }, kParGrain);
+    for (int c = 0; c < SG_CNT_COUNT; ++c) {
+        out->total[c] = 0;
+        for (size_t t = 0; t < 64; ++t) out->total[c] += part[t * SG_CNT_COUNT + c];
+    }
 }
 
 // ------------------------------------------------------------ K5: shards over devices
@@ -1327,10 +1626,20 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
 
     bool mixed = false;
     int64_t lmin = INT64_MAX, lmax = 0;
-    for (int64_t k = 0; k < n; ++k) {
-        const int64_t l = in->text_len[k] + in->pat_len[k];
-        lmin = std::min(lmin, l);
-        lmax = std::max(lmax, l);
+    {
+        std::vector<int64_t> pmin(64, INT64_MAX), pmax(64, 0);
+        parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
+            int64_t a = INT64_MAX, b = 0;
+            for (int64_t k = lo; k < hi; ++k) {
+                const int64_t l = in->text_len[k] + in->pat_len[k];
+                a = std::min(a, l);
+                b = std::max(b, l);
+            }
+            pmin[static_cast<size_t>(t)] = a;
+            pmax[static_cast<size_t>(t)] = b;
+        }, kParGrain);
+        lmin = *std::min_element(pmin.begin(), pmin.end());
+        lmax = *std::max_element(pmax.begin(), pmax.end());
     }
     mixed = n > 1 && lmax != lmin;
     // One device: the run bytes leave in slices while K1 still runs (§5). Slices are
@@ -1366,6 +1675,13 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             const int64_t sn = plan.gathered ? static_cast<int64_t>(plan.members[d].size())
                                              : plan.cut[d + 1] - plan.cut[d];
             const int32_t* st = so[d].status.as<int32_t>();
+            if (!plan.gathered) {  // contiguous shards: the first bad pair was found at the fetch
+                if (so[d].first_bad >= 0 && (bad < 0 || plan.cut[d] + so[d].first_bad < bad)) {
+                    bad = plan.cut[d] + so[d].first_bad;
+                    bad_status = so[d].first_bad_status;
+                }
+                continue;
+            }
             for (int64_t k = 0; k < sn; ++k) {
                 if (!st[k]) continue;
                 const int64_t g = plan.gathered ? plan.members[d][static_cast<size_t>(k)] : plan.cut[d] + k;
@@ -1452,25 +1768,44 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             RunConfig rcs = rcfg;
             rcs.band = rcfg.band && band_pays(s.in, s.lo, s.hi, rcfg.W, rcfg.O);
             const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
-            prep_shard(s, prep[d], mixed && !(sliced && uniform), split);
+            const int64_t words[2] = {wlo, whi};
+            prep_shard(s, prep[d], mixed && !(sliced && uniform), split, words);
             o.h2d_bytes += upload_shard(st, s, prep[d], streamed, true);
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "upload", since_ms(t0));
             const int64_t sn = s.hi - s.lo;
             int slices = 0;
             int32_t per = 0;
-            // (K1 mixed finishes every pair with a tail window after its own launch,
-            // so no slice would be ready early: one K2/K3 and one D2H instead)
+            // (K1 mixed leaves every pair's tail to the launches after it: pipelined,
+            // they run per slice beside it on a few SMs, §3.12)
             if (sliced && !rcs.band) {
                 slices = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices, std::max<int64_t>(1, sn / 4096)));
                 per = static_cast<int32_t>((sn + slices - 1) / slices);
                 slices = static_cast<int>((sn + per - 1) / per);
+            } else if (sliced && !(opt.diagnostics & SG_DIAG_NO_PIPELINE) && !prep[d].ordered &&
+                       st.sms >= 16 && tail_sm_count(st, rcs, prep[d]) * 10 <= st.sms) {
+                // K1 mixed, pipelined (§3.12). Its lanes take the pairs in input order
+                // and, the pairs being of near-equal length, finish them round by
+                // round: the pairs of all rounds but the last leave it early and go
+                // out in slices; those of the last round are one slice, run on the
+                // whole device when K1 mixed ends. (Batches whose tail / final windows
+                // are a large share of the work, cfg2: the kernels one after another
+                // on every SM are faster than a static split of the SMs.)
+                const int64_t lanes = std::max<int64_t>(
+                    1, 32 * band_active_warps(st, rcs, sn, st.sms - tail_sm_count(st, rcs, prep[d])));
+                const int64_t early = (sn / lanes - 1) * lanes;
+                if (early >= 4096) {
+                    const int es = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices - 1, early / 4096));
+                    per = static_cast<int32_t>((early + es - 1) / es);
+                    slices = es + 1;
+                }
             }
             o.launches = launch_shard(st, rcs, prep[d], slices, per);
+            fetch_small_issue(st, prep[d].n, o);  // (beside the last slices' run bytes)
             if (slices) {
                 stream_runs(st, slices, prep[d].scratch_bytes, o);
                 if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "runs d2h", since_ms(t0));
             }
-            fetch_small(st, prep[d].n, o);
+            fetch_small_finish(st, prep[d].n, o);
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "kernels", since_ms(t0));
         });
         meet.arrive(size_results);

@@ -840,6 +840,25 @@ __device__ __forceinline__ int q_pop_warp(uint32_t* q, int cap, bool want) {
     return static_cast<int>(v) - 1;
 }
 
+// K1 mixed's lists of pairs it leaves to the launches after it (the tail K1's t_list,
+// the full-frame K1's u_list). Pipelined launches (P.body_done) keep
+// one list and one count per output slice — slice sl's region starts at entry sl *
+// slice_pairs, the last slice takes the rest of the pairs — and count the pairs of
+// each slice that have left the mixed kernel:
+// the slice's tail K1 starts once its count is complete (k1_tail's wait).
+__device__ __forceinline__ void body_left(const AlignParams& P, int pair) {
+    if (!P.body_done) return;
+    __threadfence();  // the pair's state and its list entry before the count
+    atomicAdd(P.body_done + min(pair / P.slice_pairs, P.last_slice), 1u);
+}
+__device__ __forceinline__ void list_push(const AlignParams& P, bool tail, int pair) {
+    const int sl = P.body_done ? min(pair / P.slice_pairs, P.last_slice) : 0;
+    int32_t* const list = (tail ? P.t_list : P.u_list) +
+                          (P.body_done ? static_cast<long long>(sl) * P.slice_pairs : 0ll);
+    list[atomicAdd((tail ? P.t_count : P.u_count) + sl, 1u)] = pair;
+    body_left(P, pair);
+}
+
 // The K1 window loop of one warp. BAND = true: the band frame (K1b) — windows
 // it cannot take (final windows, n_w < W, |m_w - n_w| > 30, D(0, 0) > 30) go
 // with the pair to a full-frame warp (P.mixed); a full-frame warp hands the
@@ -887,7 +906,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     const int step_limit = W - P.O;
     const int K = P.single ? P.k_single : W;  // edit budget: rows 0..K
     // fresh pairs of this launch (a device count when a pre-pass split the batch)
-    const int n_fresh = P.n_fresh ? *P.n_fresh : P.n_pairs;
+    // (read through L2: a pipelined launch's count was written by K1 mixed running beside it)
+    int n_fresh = P.n_pairs;
+    if (P.n_fresh) n_fresh = __ldcg(P.n_fresh);
     // band pass: traceback-event columns, last exact row, shift multipliers
     const int cmax = BAND ? step_limit : C;
     const int band_last = min(K, band::kLastRow);
@@ -1293,7 +1314,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         rs[2] = (cur_op & 0xFF) | (cur_len << 8);
         rs[3] = static_cast<int32_t>(acc);
         if (BAND && hand_to == 5) {  // the tail K1 resumes the pair (its STD window)
-            P.t_list[atomicAdd(P.t_count, 1u)] = pair;
+            list_push(P, true, pair);
             if (P.mixed) atomicSub(P.remaining, 1u);
             return;
         }
@@ -1302,7 +1323,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             // tail (§3.10), or all of it (K0: the first window already has D(0, 0) >
             // 30, an unrelated pair whose every window would go to a cooperative
             // warp, or is not band-shaped at all)
-            P.u_list[atomicAdd(P.u_count, 1u)] = pair;
+            list_push(P, false, pair);
             if (P.mixed) atomicSub(P.remaining, 1u);
             return;
         }
@@ -1344,6 +1365,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             __threadfence();
             atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
         }
+        body_left(P, pair);
         if (P.mixed) atomicSub(P.remaining, 1u);
     };
 
@@ -2195,6 +2217,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                     __threadfence();
                     atomicAdd(P.slice_done + pair / P.slice_pairs, 1u);
                 }
+                body_left(P, pair);
                 atomicSub(P.remaining, 1u);
                 atomicSub(P.coop_out, 1u);
             } else {
@@ -2213,7 +2236,7 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
                 r[2] = (cur_op & 0xFF) | (cur_len << 8);
                 r[3] = static_cast<int32_t>(acc);
                 if (hand == 5) {
-                    P.t_list[atomicAdd(P.t_count, 1u)] = pair;
+                    list_push(P, true, pair);
                     atomicSub(P.remaining, 1u);
                     atomicSub(P.coop_out, 1u);
                 } else {
@@ -2280,6 +2303,25 @@ __global__ void __launch_bounds__(32 * kMixedWarps, 1)
 __global__ void __launch_bounds__(32 * band::WARPS, 1) k1_tail(const __grid_constant__ AlignParams P) {
     extern __shared__ uint32_t smem[];
     const int wib = threadIdx.x >> 5;
+    if (P.wait_count) {
+        // pipelined launch (§3.12): this slice's pairs are still leaving K1 mixed, which
+        // runs beside this kernel on the other SMs and never waits for it. The wait is
+        // bounded: a count that stays short is an internal error, not a hang.
+        if (threadIdx.x == 0) {
+            unsigned long long t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (*reinterpret_cast<const volatile unsigned*>(P.wait_count) < P.wait_target) {
+                __nanosleep(2000);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 60000000000ull) {  // 60 s
+                    atomicExch(P.pipe_err, 1u);
+                    break;
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
     k1_body<2, true, true>(P, smem + wib * k1_warp_words<2, true>(),
                            static_cast<long long>(blockIdx.x) * band::WARPS + wib, nullptr, nullptr);
 }
@@ -2413,7 +2455,9 @@ __global__ void __launch_bounds__(kSliceBlock)
     __shared__ long long carry;
     if (threadIdx.x == 0) {
         const unsigned want = static_cast<unsigned>(hi - lo);
-        while (*reinterpret_cast<const volatile unsigned*>(slice_done + s) < want) __nanosleep(2000);
+        // (null: the launches before this one on the stream finished the slice, §3.12)
+        while (slice_done && *reinterpret_cast<const volatile unsigned*>(slice_done + s) < want)
+            __nanosleep(2000);
         __threadfence();
         carry = lo == 0 ? 0 : dense_off[lo];
     }

@@ -96,6 +96,16 @@ struct AlignParams {
     // counts are complete when its slice's count includes it (null: no slices)
     unsigned int* slice_done;
     int32_t slice_pairs;      // pairs per slice (pair k is in slice k / slice_pairs)
+    // pipelined launches (§3.12): K1 mixed on most SMs, the tail / full-frame K1 of each
+    // output slice beside it on the SMs it leaves free. K1 mixed: t_list / u_list hold one
+    // region of slice_pairs entries per slice, t_count / u_count one count per slice, and
+    // body_done[sl] counts the pairs of slice sl that have left it (null: one list each).
+    // The tail K1 of a slice starts once *wait_count >= wait_target (null: at once).
+    unsigned int* body_done;
+    int32_t last_slice;       // pairs from last_slice * slice_pairs on are one slice
+    const unsigned int* wait_count;
+    unsigned int wait_target;
+    unsigned int* pipe_err;   // set when such a wait timed out (the host fails the call)
     unsigned long long* phase_cycles;  // optional [8]: phase cycles and counts (diagnostics)
     unsigned long long* warp_times;    // optional [warps][2]: start / exit globaltimer, smid (diagnostics)
 };
