@@ -43,3 +43,41 @@ def test_whole_config_digests(gpu, name, cfg, W, Ov, s, d, e, kernel):
     bad = [(b0, cnt) for (b0, cnt, want), have in zip(blocks, got) if want != have]
     assert not bad, f"{name} [{kernel}]: {len(bad)} of {len(blocks)} blocks differ, first {bad[:5]}"
     assert tot == total
+
+
+def _check_digests(name, res):
+    blocks, pairs, total, cells = G.read_digests(name)
+    assert int(res.total.cells_computed) == cells
+    got, tot = O.results_digests(res)
+    bad = [(b0, cnt) for (b0, cnt, want), have in zip(blocks, got) if want != have]
+    assert not bad, f"{name}: {len(bad)} of {len(blocks)} blocks differ, first {bad[:5]}"
+    assert tot == total
+
+
+def test_pipelined_launches_cfg3(gpu):
+    """One-shot calls of long-read batches run the tail kernels beside K1 mixed, per
+    output slice. The same call with SG_DIAG_NO_PIPELINE launches
+    them after it: both must reproduce the reference's digests of every pair."""
+    sg = gpu
+    batch = _batch(sg, 3)
+    config = sg.AlignerConfig(W=64, O=24)
+    piped = sg.align_packed(config, batch)
+    assert piped.gpu_launches > 16, "cfg3 should take the pipelined launches"
+    _check_digests("cfg3.tsv", piped)
+    with sg.options(diagnostics=8):
+        plain = sg.align_packed(config, batch)
+    assert plain.gpu_launches <= 8
+    _check_digests("cfg3.tsv", plain)
+    assert (piped.runs == plain.runs).all() and (piped.cigar_off == plain.cigar_off).all()
+
+
+def test_pipelined_launches_unrelated_pairs(gpu):
+    """cfg5 in input order through the pipelined mixed kernel: pairs of 100..20k bases,
+    30 % unrelated — every slice has a tail list and a K0 list (unrelated pairs from
+    their start, final windows), and the slices finish out of step."""
+    sg = gpu
+    batch = _batch(sg, 5)
+    with sg.options(kernel="mixed", longest_first=False):
+        res = sg.align_packed(sg.AlignerConfig(W=64, O=24), batch)
+    assert res.gpu_launches > 16, "cfg5 in input order should take the pipelined launches"
+    _check_digests("cfg5.tsv", res)
