@@ -993,11 +993,27 @@ int tail_sm_count(const DevState& st, const RunConfig& rc, const ShardPrep& pp) 
     return std::max(2, std::min(t, st.sms / 2));
 }
 
+// Output slices of a one-shot call (§3.12, §5): `early` slices of `per` pairs, then
+// (K1 mixed, pipelined: the pairs of its last round) `late` slices of `per_late` pairs,
+// the final one taking the rest.
+struct SlicePlan {
+    int early = 0, late = 0;
+    int32_t per = 0, per_late = 0;
+    int total() const { return early + late; }
+    int64_t early_pairs(int64_t n) const { return std::min<int64_t>(n, int64_t{early} * per); }
+    int64_t lo(int sl, int64_t n) const {
+        if (sl < early) return std::min<int64_t>(n, int64_t{sl} * per);
+        return std::min<int64_t>(n, early_pairs(n) + int64_t{sl - early} * per_late);
+    }
+    int64_t hi(int sl, int64_t n) const { return sl == total() - 1 ? n : lo(sl + 1, n); }
+};
+
 // Events: ev[0] before K1, ev[1] after K1, ev[2] after K3. Returns launches.
 // slices > 0 (one-shot calls): K2/K3 run per slice of `slice_pairs` pairs on the
 // slice stream while K1 runs; ev_slice[s] marks slice s's bytes dense on the device.
-int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int slices = 0,
-                 int32_t slice_pairs = 0) {
+int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const SlicePlan& plan = SlicePlan{}) {
+    const int slices = plan.total();
+    const int32_t slice_pairs = plan.per;
     const int64_t n = pp.n;
     const size_t n1 = static_cast<size_t>(std::max<int64_t>(n, 1));
     st.distance.ensure(4 * n1);
@@ -1138,7 +1154,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
             p.t_count = ctr + DevState::kPipeT;
             p.u_count = ctr + DevState::kPipeU;
             p.body_done = ctr + DevState::kPipeBody;
-            p.last_slice = slices - 1;
+            p.last_slice = slices - 1;  // (late slices are `per` pairs too: one division per pair)
             p.pipe_err = ctr + DevState::kPipeErr;
             // everything the slice stream's kernels read is set up before they start
             SG_CUDA_CHECK(cudaEventRecord(st.slice_go, st.stream));
@@ -1150,10 +1166,9 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
             int64_t* info = nullptr;
             SG_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&info), st.slice_info, 0));
             for (int sl = 0; sl < slices; ++sl) {
-                const int32_t lo = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl} * slice_pairs));
+                const int32_t lo = static_cast<int32_t>(plan.lo(sl, n));
                 const bool last = sl == slices - 1;
-                const int32_t hi = last ? static_cast<int32_t>(n)
-                                        : static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl + 1} * slice_pairs));
+                const int32_t hi = static_cast<int32_t>(plan.hi(sl, n));
                 // the slice's STD windows, once its pairs have left K1 mixed: on the SMs
                 // K1 mixed leaves free (the last slice: on every SM, K1 mixed is ending)
                 sgk::AlignParams pt = p;
@@ -1170,8 +1185,14 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
                 pt.u_count = ctr + DevState::kPipeU + sl;
                 pt.wait_count = ctr + DevState::kPipeBody + sl;
                 pt.wait_target = static_cast<unsigned>(hi - lo);
+                // (slices of the last round: K1 mixed's blocks are leaving, the grids grow
+                // towards the whole device)
+                int tgrid = last ? st.sms : tsm;
+                if (sl >= plan.early && !last)
+                    tgrid = tsm + static_cast<int>(static_cast<long long>(st.sms - tsm) * (sl - plan.early + 1) /
+                                                   plan.late);
                 SG_CUDA_CHECK(static_cast<cudaError_t>(
-                    sgk::launch_tail_align(pt, last ? st.sms : tsm, st.slice_stream)));
+                    sgk::launch_tail_align(pt, tgrid, st.slice_stream)));
                 // then the full-frame K1 over the slice's list: final windows, unrelated pairs
                 sgk::AlignParams pu = p;
                 pu.warp_times = nullptr;
@@ -1183,7 +1204,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
                 pu.n_fresh = reinterpret_cast<const int32_t*>(ctr + DevState::kPipeU + sl);
                 pu.next_pair = ctr + DevState::kPipeFullQ + sl;
                 pu.restore = 1;
-                const long long gfull = last ? grid : std::min<long long>(grid, static_cast<long long>(tsm) * full_bps);
+                const long long gfull = last ? grid : std::min<long long>(grid, static_cast<long long>(tgrid) * full_bps);
                 SG_CUDA_CHECK(static_cast<cudaError_t>(
                     sgk::launch_window_align(rc.L, pu, static_cast<int>(gfull), wpb, st.slice_stream)));
                 if (last) SG_CUDA_CHECK(cudaEventRecord(st.k1_done, st.slice_stream));
@@ -1241,8 +1262,8 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, int sli
     if (slices > 0) {
         SG_CUDA_CHECK(cudaStreamWaitEvent(st.slice_stream, st.slice_go, 0));
         for (int sl = 0; sl < slices; ++sl) {
-            const int32_t lo = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl} * slice_pairs));
-            const int32_t hi = static_cast<int32_t>(std::min<int64_t>(n, int64_t{sl + 1} * slice_pairs));
+            const int32_t lo = static_cast<int32_t>(plan.lo(sl, n));
+            const int32_t hi = static_cast<int32_t>(plan.hi(sl, n));
             int64_t* info = nullptr;
             SG_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&info), st.slice_info, 0));
             SG_CUDA_CHECK(static_cast<cudaError_t>(sgk::launch_slice_scan(
@@ -1286,6 +1307,13 @@ struct ShardOut {
     int64_t h2d_bytes = 0, d2h_bytes = 0;
 };
 
+thread_local const std::chrono::steady_clock::time_point* g_trace_t0 = nullptr;  // SG_DIAG_HOST_TRACE
+void trace_point(const char* what) {
+    if (g_trace_t0)
+        std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - *g_trace_t0).count());
+}
+
 // Issues the D2H of a shard's small per-pair outputs on its main stream (they wait
 // for every kernel there); fetch_small_finish waits for them.
 void fetch_small_issue(DevState& st, int64_t n, ShardOut& so) {
@@ -1316,6 +1344,7 @@ void fetch_small_issue(DevState& st, int64_t n, ShardOut& so) {
 
 void fetch_small_finish(DevState& st, int64_t n, ShardOut& so) {
     SG_CUDA_CHECK(cudaStreamSynchronize(st.stream));
+    trace_point("small d2h");
     if (*so.pipe_err.as<unsigned>()) {
         set_error(SG_INTERNAL, "device pipeline: a slice's tail launch timed out waiting for K1 mixed");
         throw Fail{SG_INTERNAL};
@@ -1359,6 +1388,7 @@ void stream_runs(DevState& st, int slices, int64_t bound_total, ShardOut& o) {
     int64_t end = 0;
     for (int sl = 0; sl < slices; ++sl) {
         SG_CUDA_CHECK(cudaEventSynchronize(st.ev_slice[sl]));
+        if (sl == slices - 1) trace_point("last k3");
         const volatile int64_t* info = st.slice_info;
         const int64_t base = info[2 * sl], bytes = info[2 * sl + 1];
         if (base + bytes > static_cast<int64_t>(o.runs.cap)) {
@@ -1619,6 +1649,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     DeviceGuard guard;
     const sg_options opt = options();
     const bool trace = (opt.diagnostics & SG_DIAG_HOST_TRACE) != 0;
+    g_trace_t0 = trace && n_devices == 1 ? &t0 : nullptr;
     const RunConfig rcfg = run_config(cfg, n, in->text_len, in->pat_len);
     const size_t nd = static_cast<size_t>(n_devices);
     const ShardPlan plan = plan_shards(in, nd);
@@ -1773,33 +1804,44 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             o.h2d_bytes += upload_shard(st, s, prep[d], streamed, true);
             if (trace) std::fprintf(stderr, "[sg trace] %-10s %8.2f ms\n", "upload", since_ms(t0));
             const int64_t sn = s.hi - s.lo;
-            int slices = 0;
-            int32_t per = 0;
+            SlicePlan sp;
             // (K1 mixed leaves every pair's tail to the launches after it: pipelined,
             // they run per slice beside it on a few SMs, §3.12)
             if (sliced && !rcs.band) {
-                slices = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices, std::max<int64_t>(1, sn / 4096)));
-                per = static_cast<int32_t>((sn + slices - 1) / slices);
-                slices = static_cast<int>((sn + per - 1) / per);
+                sp.early = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices, std::max<int64_t>(1, sn / 4096)));
+                sp.per = static_cast<int32_t>((sn + sp.early - 1) / sp.early);
+                sp.early = static_cast<int>((sn + sp.per - 1) / sp.per);
             } else if (sliced && !(opt.diagnostics & SG_DIAG_NO_PIPELINE) && !prep[d].ordered &&
                        st.sms >= 16 && tail_sm_count(st, rcs, prep[d]) * 10 <= st.sms) {
                 // K1 mixed, pipelined (§3.12). Its lanes take the pairs in input order
                 // and, the pairs being of near-equal length, finish them round by
                 // round: the pairs of all rounds but the last leave it early and go
-                // out in slices; those of the last round are one slice, run on the
-                // whole device when K1 mixed ends. (Batches whose tail / final windows
-                // are a large share of the work, cfg2: the kernels one after another
-                // on every SM are faster than a static split of the SMs.)
+                // out in slices of >= 4096 pairs; those of the last round finish while
+                // K1 mixed's blocks leave, in slices of the same size on growing grids. (Batches whose tail / final windows are a large share of the
+                // work, cfg2: the kernels one after another on every SM are faster than
+                // a static split of the SMs.)
                 const int64_t lanes = std::max<int64_t>(
                     1, 32 * band_active_warps(st, rcs, sn, st.sms - tail_sm_count(st, rcs, prep[d])));
                 const int64_t early = (sn / lanes - 1) * lanes;
                 if (early >= 4096) {
-                    const int es = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices - 1, early / 4096));
-                    per = static_cast<int32_t>((early + es - 1) / es);
-                    slices = es + 1;
+                    // (the last round in slices of the same size: a second slice size
+                    // in K1 mixed's pair -> slice mapping cost its window loop 2 %)
+                    int es = static_cast<int>(std::min<int64_t>(DevState::kMaxSlices - 1, early / 4096));
+                    int32_t per = static_cast<int32_t>((early + es - 1) / es);
+                    while ((sn + per - 1) / per > DevState::kMaxSlices && es > 1) {
+                        --es;
+                        per = static_cast<int32_t>((early + es - 1) / es);
+                    }
+                    const int64_t tot = (sn + per - 1) / per;
+                    if (tot <= DevState::kMaxSlices && tot > es) {
+                        sp.early = es;
+                        sp.per = sp.per_late = per;
+                        sp.late = static_cast<int>(tot) - es;
+                    }
                 }
             }
-            o.launches = launch_shard(st, rcs, prep[d], slices, per);
+            const int slices = sp.total();
+            o.launches = launch_shard(st, rcs, prep[d], sp);
             fetch_small_issue(st, prep[d].n, o);  // (beside the last slices' run bytes)
             if (slices) {
                 stream_runs(st, slices, prep[d].scratch_bytes, o);
