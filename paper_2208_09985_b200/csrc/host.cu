@@ -667,6 +667,58 @@ bool band_pays(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W, int O) 
     return unrelated * 20 <= tested;
 }
 
+// Expected edits per window of W columns, from a strided sample of <= 16 pairs: the share
+// r of exact 8-base blocks of the first 256 text bases found in the pattern within +-16
+// diagonals estimates the per-base identity as r^(1/8) (cfg2, 2 % edits: r ~ 0.85; cfg3,
+// 15 %: r ~ 0.27). Only K1 mixed's chunk schedule depends on it (band_subchunks), never
+// a result. Returns -1 when no sampled pair is long enough.
+double expected_window_edits(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W) {
+    const int64_t n = hi - lo;
+    const int64_t samples = std::min<int64_t>(n, 16);
+    int64_t blocks = 0, hits = 0;
+    for (int64_t i = 0; i < samples; ++i) {
+        const int64_t k = lo + i * n / samples;
+        const int64_t nt = in->text_len[k], m = in->pat_len[k];
+        const int64_t len = std::min<int64_t>(std::min(nt, m), 256);
+        if (len < 64) continue;
+        const int64_t ta = in->text_off[k], pa = in->pat_off[k];
+        for (int64_t b = 0; b + 8 <= len; b += 8) {
+            const uint32_t t = bases8(in->seq, ta + b);
+            ++blocks;
+            for (int64_t dl = -16; dl <= 16; ++dl) {
+                const int64_t j = b + dl;
+                if (j < 0 || j + 8 > m) continue;
+                if (bases8(in->seq, pa + j) == t) {
+                    ++hits;
+                    break;
+                }
+            }
+        }
+    }
+    if (blocks < 8) return -1.0;
+    const double r = std::max(1e-3, static_cast<double>(hits) / static_cast<double>(blocks));
+    return W * (1.0 - std::pow(r, 1.0 / 8.0));
+}
+
+// K1 mixed's band chunks per phase (§3.8): one 8-row chunk when the windows are expected
+// to hold fewer than 4.5 edits and the pairs are at least three windows long, else the
+// default two. K1 on one B200, two chunks -> one: cfg2 (1.3 edits expected) 5.52 -> 4.97
+// ms, cfg4 W = 32 (3.2) 5.42 -> 4.19; the other way cfg4 W = 64 (6.4) 4.62 -> 4.78, cfg3
+// (9.6) 17.7 -> 22.4.
+int band_schedule(const sg_packed_pairs* in, int64_t lo, int64_t hi, int W) {
+    const int64_t n = hi - lo;
+    if (n <= 0) return 0;
+    const int64_t samples = std::min<int64_t>(n, 16);
+    double len = 0;
+    for (int64_t i = 0; i < samples; ++i) {
+        const int64_t k = lo + i * n / samples;
+        len += static_cast<double>(std::max(in->text_len[k], in->pat_len[k]));
+    }
+    if (len / static_cast<double>(samples) < 3.0 * W) return 0;
+    const double e = expected_window_edits(in, lo, hi, W);
+    return e >= 0 && e < 4.5 ? 1 : 0;
+}
+
 // Host-side per-pair inputs of a shard: rebased offsets, lengths, bounds, order.
 struct ShardPrep {
     PinBuf text_off, pat_off, text_len, pat_len, has_n, bound_off, order;
@@ -813,6 +865,7 @@ struct RunConfig {
     int L, W, O, et, policy, single, k_single;
     bool wide;  // K6 (one warp per pair): windows wider than 128 bits
     bool band;  // K1b band pass first, full-frame K1 resumes what it defers (§3.8)
+    int band_sub = 0;  // K1 mixed: band chunks per phase (0: the kernel's default)
     int wcap;   // K6: widest window in columns
 };
 
@@ -1127,6 +1180,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const S
         // back (§3.8)
         p.mixed = 1;
         p.band_active = static_cast<int32_t>(band_warps);
+        p.band_subchunks = rc.band_sub;
         p.q_band = st.q_band.as<uint32_t>();
         p.q_full = st.q_full.as<uint32_t>();
         p.q_coop = st.q_coop.as<uint32_t>();
@@ -1181,6 +1235,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const S
                 pt.next_pair = ctr + DevState::kPipeTailQ + sl;
                 pt.restore = 1;
                 pt.band_active = 0x7FFFFFFF;
+                pt.band_subchunks = 0;
                 pt.u_list = st.u_list.as<int32_t>() + lo;
                 pt.u_count = ctr + DevState::kPipeU + sl;
                 pt.wait_count = ctr + DevState::kPipeBody + sl;
@@ -1237,6 +1292,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const S
         pt.next_pair = st.next_pair.as<unsigned int>() + 4;
         pt.restore = 1;
         pt.band_active = 0x7FFFFFFF;
+        pt.band_subchunks = 0;  // (STD windows: D ~ 48, the default schedule)
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_tail_align(pt, static_cast<int>(st.sms), st.stream)));
         sgk::AlignParams pu = p;
@@ -1798,6 +1854,7 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
             o.h2d_bytes = upload_seq(st, s, wlo, whi, streamed);
             RunConfig rcs = rcfg;
             rcs.band = rcfg.band && band_pays(s.in, s.lo, s.hi, rcfg.W, rcfg.O);
+            if (rcs.band) rcs.band_sub = band_schedule(s.in, s.lo, s.hi, rcfg.W);
             const int64_t split = streamed ? pairs_in_flight(st, rcs, s.hi - s.lo) : 0;
             const int64_t words[2] = {wlo, whi};
             prep_shard(s, prep[d], mixed && !(sliced && uniform), split, words);
@@ -2151,6 +2208,7 @@ int sg_session_create(const sg_config* cfg, const sg_packed_pairs* pairs, int de
         s->cfg = *cfg;
         s->rc = run_config(cfg, pairs->n_pairs, pairs->text_len, pairs->pat_len);
         s->rc.band = s->rc.band && band_pays(pairs, 0, pairs->n_pairs, s->rc.W, s->rc.O);
+        if (s->rc.band) s->rc.band_sub = band_schedule(pairs, 0, pairs->n_pairs, s->rc.W);
         s->st.init(device);
         s->n = pairs->n_pairs;
         bool mixed = false;

@@ -912,6 +912,10 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
     // band pass: traceback-event columns, last exact row, shift multipliers
     const int cmax = BAND ? step_limit : C;
     const int band_last = min(K, band::kLastRow);
+    // band chunks per phase: kBandSubChunks (16 rows) unless the host expects windows of
+    // a few edits (cfg2, cfg4 W = 32: one 8-row chunk solves nearly every window, and a
+    // second one would run for the whole warp whenever one lane needs it)
+    const int band_sub = P.band_subchunks > 0 ? P.band_subchunks : kBandSubChunks;
     const uint32_t hmul = two << 30;  // 2^31 at run time: mul.hi(x, hmul) = x >> 1
 
     // ---- lane state ----
@@ -1544,7 +1548,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
         // that more lanes reach it together; solved lanes sweep idle.
         bool solved = false;
         const int n_in = BAND ? 0 : __popc(__ballot_sync(kFull, in_dc));
-        for (int sub = 0; sub < (BAND ? kBandSubChunks : kSubMax); ++sub) {
+        for (int sub = 0; sub < (BAND ? band_sub : kSubMax); ++sub) {
             const bool act = in_dc && !solved;
             if (BAND) {
                 if (sub > 0 && !__any_sync(kFull, act)) break;

@@ -79,6 +79,7 @@ struct AlignParams {
     // K1 mixed: band warps (K1b) <-> full-frame warps
     int32_t mixed;
     int32_t band_active;      // band warps that take pairs (spread over the blocks)
+    int32_t band_subchunks;   // band chunks per phase (0: the default, 16 rows)
     uint32_t* q_band;         // pairs handed to band warps: [32 + n_pairs] (head, tail, slots)
     uint32_t* q_full;         // pairs handed to full-frame warps
     uint32_t* q_coop;         // pairs handed to the cooperative warps (one window per warp)
