@@ -1706,6 +1706,9 @@ int align_packed_impl(const sg_config* cfg, const sg_packed_pairs* in, const int
     const sg_options opt = options();
     const bool trace = (opt.diagnostics & SG_DIAG_HOST_TRACE) != 0;
     g_trace_t0 = trace && n_devices == 1 ? &t0 : nullptr;
+    struct TraceReset {  // (t0 is this call's: no trace point may outlive it)
+        ~TraceReset() { g_trace_t0 = nullptr; }
+    } trace_reset;
     const RunConfig rcfg = run_config(cfg, n, in->text_len, in->pat_len);
     const size_t nd = static_cast<size_t>(n_devices);
     const ShardPlan plan = plan_shards(in, nd);

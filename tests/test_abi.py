@@ -141,3 +141,21 @@ def test_single_window_length_limits(sg):
     except sg.CudaError:
         pass
     cfg.validate()  # single-window configs without DENT are valid
+
+
+def test_first_bad_pair_of_a_large_batch(sg):
+    """batch.cpp:18-25 names the first failing pair in input order. The length checks of a
+    large batch run on the library's worker pool in chunks: the lowest index must still be
+    the one reported, whichever chunk finds its bad pair first."""
+    batch = sg.synth_packed(1, 0, 200000)
+    tl, pl = batch.lengths()
+    saved = (int(tl[150001]), int(pl[60002]), int(pl[199999]))
+    try:
+        tl[150001] = 0
+        pl[60002] = 0
+        pl[199999] = 0
+        for _ in range(20):  # (any worker may reach its chunk's bad pair first)
+            with pytest.raises(sg.InputError, match=r"pair '60002': empty sequence"):
+                sg.align_packed(sg.AlignerConfig(W=64, O=24), batch)
+    finally:
+        tl[150001], pl[60002], pl[199999] = saved
