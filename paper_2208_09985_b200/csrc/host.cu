@@ -1006,6 +1006,14 @@ long long k1_grid(const DevState& st, const RunConfig& rc, int64_t n, bool band_
     return std::max(1LL, std::min(grid, max_grid));
 }
 
+// Band chunks per phase of the tail K1: its STD windows need rows 0..D with D ~ 33-64
+// (a text of W bases against <= 31 pattern bases), so every lane runs chunk after chunk
+// and the traceback phase waits until the warp has none left to run.
+#ifndef SG_TAIL_SUB
+#define SG_TAIL_SUB 8
+#endif
+constexpr int kTailSubChunks = SG_TAIL_SUB;
+
 // K1 mixed: band warps that take pairs, spread over one block per SM; the others
 // exit at once. Every slot when there are more pairs than lanes: unlike the
 // full-frame kernel, whole rounds do not pay here (cfg3 100k: 3.02 rounds on all
@@ -1235,7 +1243,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const S
                 pt.next_pair = ctr + DevState::kPipeTailQ + sl;
                 pt.restore = 1;
                 pt.band_active = 0x7FFFFFFF;
-                pt.band_subchunks = 0;
+                pt.band_subchunks = kTailSubChunks;
                 pt.u_list = st.u_list.as<int32_t>() + lo;
                 pt.u_count = ctr + DevState::kPipeU + sl;
                 pt.wait_count = ctr + DevState::kPipeBody + sl;
@@ -1292,7 +1300,7 @@ int launch_shard(DevState& st, const RunConfig& rc, const ShardPrep& pp, const S
         pt.next_pair = st.next_pair.as<unsigned int>() + 4;
         pt.restore = 1;
         pt.band_active = 0x7FFFFFFF;
-        pt.band_subchunks = 0;  // (STD windows: D ~ 48, the default schedule)
+        pt.band_subchunks = kTailSubChunks;  // (STD windows: D ~ 48, rows 0..D in one phase)
         SG_CUDA_CHECK(static_cast<cudaError_t>(
             sgk::launch_tail_align(pt, static_cast<int>(st.sms), st.stream)));
         sgk::AlignParams pu = p;

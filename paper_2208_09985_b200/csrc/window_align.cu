@@ -20,7 +20,11 @@ constexpr unsigned kFull = 0xffffffffu;
 // (warps are independent; blocks only share an SM).
 template <int L> struct KCfg;
 template <> struct KCfg<1> { static constexpr int R = 4, C = 32, WARPS = 4, MINB = 2; };
-template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4, MINB = 3; };
+// (L = 2: two blocks of four warps per SM and up to 255 registers. With three blocks, 12
+// warps at 168 registers, the sweep state spilled to a 128-byte stack frame: cfg5 127 ->
+// 105 ms, cfg2's final-window pass 1.67 -> 1.3 ms, cfg4 W = 64 in this kernel 12.5 -> 9.8;
+// 6, 9, 10 warps per SM: 124, 114, 123 ms.)
+template <> struct KCfg<2> { static constexpr int R = 4, C = 40, WARPS = 4, MINB = 2; };
 // (L = 4: C covers W - O = 80 of cfg4's W = 128, O = 48; with 32 columns every such
 // window ran as three continuation segments, 2.7 x the DC chunks)
 #ifndef SG_C4
