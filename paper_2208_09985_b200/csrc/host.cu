@@ -793,14 +793,12 @@ void prep_shard(const Shard& s, ShardPrep& pp, bool longest_first, int64_t split
     };
     // two passes over contiguous chunks: each chunk's bound total, then its pairs
     // from the chunk's base
-    std::vector<int64_t> cbound(65, 0), clo(64, 0), chi(64, 0);
+    std::vector<int64_t> cbound(65, 0);
     std::vector<uint8_t> cn(64, 0);
     parallel_for(n, [&](int64_t a, int64_t b, int t) {
         int64_t acc = 0;
         for (int64_t k = a; k < b; ++k) acc += bound_of(s.lo + k);
         cbound[static_cast<size_t>(t) + 1] = acc;
-        clo[static_cast<size_t>(t)] = a;
-        chi[static_cast<size_t>(t)] = b;
     }, kParGrain);
     for (size_t t = 0; t < 64; ++t) cbound[t + 1] += cbound[t];
     parallel_for(n, [&](int64_t a, int64_t b, int t) {
