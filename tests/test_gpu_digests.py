@@ -81,3 +81,37 @@ def test_pipelined_launches_unrelated_pairs(gpu):
         res = sg.align_packed(sg.AlignerConfig(W=64, O=24), batch)
     assert res.gpu_launches > 16, "cfg5 in input order should take the pipelined launches"
     _check_digests("cfg5.tsv", res)
+
+
+def test_pipelined_launches_with_n_bases_and_scrambled_pairs(gpu):
+    """A long-read batch with non-ACGT bases in some pairs and some patterns replaced by
+    unrelated sequence, through the pipelined mixed kernel, the plain launches and the
+    full-frame K1: byte-identical output (no reference digests for this batch; the
+    full-frame K1 is pinned on the same shapes by the golden fixtures)."""
+    import numpy as np
+    sg = gpu
+    codes = sg.synth_codes(3, 0, 70000)
+    text, pat = codes.text.copy(), codes.pattern.copy()
+    rng = np.random.default_rng(7)
+    for k in rng.choice(codes.n, 3000, replace=False):       # N bases (code 4)
+        a, l = int(codes.text_off[k]), int(codes.text_len[k])
+        text[a + rng.integers(0, l, 5)] = 4
+        b, m = int(codes.pat_off[k]), int(codes.pat_len[k])
+        pat[b + rng.integers(0, m, 3)] = 4
+    for k in rng.choice(codes.n, 700, replace=False):        # unrelated patterns
+        b, m = int(codes.pat_off[k]), int(codes.pat_len[k])
+        pat[b:b + m] = rng.integers(0, 4, m, dtype=np.uint8)
+    batch = sg.CodesBatch(text, codes.text_off, codes.text_len, pat, codes.pat_off, codes.pat_len)
+    config = sg.AlignerConfig(W=64, O=24)
+    runs = {}
+    for name, opts in (("piped", dict(kernel="mixed")), ("plain", dict(kernel="mixed", diagnostics=8)),
+                       ("full", dict(kernel="full"))):
+        with sg.options(**opts):
+            runs[name] = sg.align_codes(config, batch)
+    assert runs["piped"].gpu_launches > 16 and runs["plain"].gpu_launches <= 8
+    ref = runs["full"]
+    for name in ("piped", "plain"):
+        r = runs[name]
+        for a, b in ((r.distance, ref.distance), (r.windows, ref.windows), (r.cigar_off, ref.cigar_off),
+                     (r.runs, ref.runs), (r.counters, ref.counters)):
+            assert np.array_equal(a, b), name
