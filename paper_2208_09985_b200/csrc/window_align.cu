@@ -1093,7 +1093,9 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
             pl[1 * 64] = lo & ~hi & valid;
             pl[2 * 64] = ~lo & hi & valid;
             pl[3 * 64] = lo & hi & valid;
-            for (int k = 0; 16 * k < n_w; ++k) {
+#pragma unroll
+            for (int k = 0; k < NW; ++k) {  // (static k: tw[] stays in registers)
+                if (16 * k >= n_w) break;
                 const int bt = t_sh + 16 * k;
                 const uint32_t tword = BAND ? tw[k]
                                             : __funnelshift_r(sq_t[(bt >> 4) * 32 + lane],
@@ -1885,7 +1887,7 @@ __device__ __forceinline__ void k1_body(const AlignParams& P, uint32_t* const wb
 // (D(0, 0) > 30, or 32 <= m_w with |m_w - n_w| > 30): 30..60 rows in one or
 // two passes instead of 8..16 sequential 4-row chunks on one lane.
 namespace coop {
-constexpr int kWords = 66 * 2 + 66 * 2 + 65 * 4 + 20;  // eq, prow, xy (+ dummies), staging
+constexpr int kWords = 66 * 2 + 66 * 2 + 65 * 4 + 20 + 8;  // eq, prow, xy (+ dummies), staging, held pairs
 }
 
 __device__ __forceinline__ uint64_t shr1_in(uint64_t x, uint32_t b) {
@@ -1914,7 +1916,10 @@ __device__ void coop_body(const AlignParams& P, uint32_t* const sm) {
         P.warp_times[dwarp * 3] = t;
         P.warp_times[dwarp * 3 + 1] = t;
     }
-    int held[8], nheld = 0, next_held = 0;  // lane 0: pairs taken in one pop
+    // lane 0: pairs taken in one pop (in shared memory: as a local array they were the
+    // kernel's only stack frame)
+    int* const held = reinterpret_cast<int*>(st + 20);
+    int nheld = 0, next_held = 0;
     for (;;) {
         int pair = -1;
         if (lane == 0) {
